@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""bench.py -- randUTV + least-squares time-to-solution and FP64 TFLOP/s on B200.
+
+Metric (BASELINE.json): "randUTV+LS time-to-solution & FP64 TFLOP/s (frac of peak),
+n=50000 @1/2/4/8".  One step = one full utv_lstsq (factor + rank + solve, all SURVEY 8(a)
+rows) on a fresh copy of the synthetic cfg3 problem (square n = 50000, rank 25000, b = 256,
+q = 2, 1 RHS; the paper's generator P:2436-2448, known min-norm solution).  `value` is the
+ALGORITHMIC FP64 rate F_alg / time (SURVEY App. B flop model, implementation independent),
+summed over ranks.  Inputs (20 GB) are far larger than the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+N > 1 (torchrun): every rank solves its own cfg3 instance (replicas, weak scaling, no data-path
+collective): the block-column-sharded strong-scaling path of SURVEY 8(e) is not built yet.
+`--impl reference`: the CPU oracle (oracle/, the only comparison program that exists for this
+paper) timed on the host cores on a bounded sample of the same recipe.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (m, n, rank, b, q, k) -- BASELINE.json configs
+    "cfg1": (512, 512, 256, 64, 1, 1),
+    "cfg2": (20000, 20000, 10000, 256, 2, 1),
+    "cfg3": (50000, 50000, 25000, 256, 2, 1),
+    "cfg4": (200000, 20000, 15000, 256, 1, 16),
+}
+METRIC = "randUTV+LS time-to-solution & FP64 TFLOP/s (frac of peak), n=50000 @1/2/4/8"
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+
+
+def f_alg(m: int, n: int, b: int, q: int, k: int, r: int) -> float:
+    """Algorithmic FP64 flops of randUTV + LS, V explicit, U not built."""
+    F = 0.0
+    j0 = 0
+    while j0 < n:
+        bw = min(b, n - j0)
+        mp, np_ = m - j0, n - j0
+        last = np_ <= b
+        if not last:
+            F += (2 + 4 * q) * mp * np_ * bw          # sketch + power iterations
+            F += 3 * np_ * bw ** 2 - (2 / 3) * bw ** 3  # QR(Y)
+            F += 4 * m * np_ * bw                     # right update, all rows
+            F += 4 * n * np_ * bw                     # V update
+        F += 3 * mp * bw ** 2 - (2 / 3) * bw ** 3     # panel QR
+        F += 4 * mp * (np_ - bw) * bw                 # left update
+        F += 4 * mp * k * bw                          # U^T B on the fly
+        F += 2 * bw ** 2 * (j0 + n + (np_ - bw) + k)  # SVD updates
+        j0 += b
+    F += r * r * k + 2 * n * r * k                    # solve
+    return F
+
+
+def fp64_peak():
+    """Measured FP64 DMMA peak (TFLOP/s) from this pool's B200 (MEASURED_PEAKS.json has no FP64)."""
+    try:
+        d = json.load(open(FP64_PEAK_FILE))
+        return float(d["microbench"]["dmma_m16n8k8_sustained_4s_tflops"]), \
+            "profiles/r01_fp64_peaks.json: mma.sync f64 (DMMA) microbenchmark, 4 s sustained"
+    except Exception:
+        return 37.2, "fallback: DMMA microbenchmark value of round 1"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(sample_n: int = 2048, threads: int | None = None):
+    """The oracle as it stands, on a bounded sample of the cfg3 recipe (rank n/2, b=256, q=2)."""
+    import numpy as np
+    import oracle
+    import utv_inputs as gen
+    if threads:
+        oracle.set_threads(threads)
+    G = gen.GpMatrix(sample_n, sample_n, sample_n // 2)
+    B, X0 = G.known_rhs(k=1)
+    t0 = time.perf_counter()
+    X, r = oracle.lstsq(G.A, B, b=256, q=2, tau=1e-10, seed=gen.SKETCH_SEED)
+    dt = time.perf_counter() - t0
+    F = f_alg(sample_n, sample_n, 256, 2, 1, r)
+    err = float(np.linalg.norm(X - X0) / np.linalg.norm(X0))
+    return {"value": F / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.get_threads(), "kind": "oracle",
+            "sample": f"oracle lstsq on the cfg3 recipe at n={sample_n} (rank {sample_n // 2}, b=256, q=2, k=1): "
+                      f"{dt:.2f} s, F_alg={F:.3e}, rel err vs x0 {err:.1e}",
+            "seconds": dt}
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return
+    import oracle
+    n_s = args.ref_n
+    times = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(n_s)
+        if i >= args.warmup:
+            times.append(cb["seconds"])
+    t = sum(times) / len(times)
+    F = f_alg(n_s, n_s, 256, 2, 1, n_s // 2)
+    val = F / t / 1e12
+    out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config} recipe, bounded CPU sample n={n_s}", "sample_n": n_s},
+           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": oracle.get_threads(), "kind": "oracle",
+                            "sample": f"oracle lstsq, cfg3 recipe at n={n_s} (rank {n_s // 2}, b=256, q=2)"},
+           "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device(f"cuda:{torch.cuda.current_device()}")
+    import paper_2408_05238_b200 as utv
+    import utv_inputs as gen
+
+    m, n, r_true, b, q, k = CONFIGS[args.config]
+    opts = utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED)
+    # synthetic cfg instance, one per rank (different seeds), column-major on the device
+    At, Bm, X0 = gen.gp_torch(m, n, r_true, seed=gen.MATRIX_SEED + rank, device=dev, k=k)
+    A0 = At.t()                                   # pristine copy, column-major m x n
+    B0 = utv.colmajor(Bm)
+    A = utv.colmajor_empty(m, n, device=dev)
+    B = utv.colmajor_empty(m, k, device=dev)
+    X = utv.colmajor_empty(n, k, device=dev)
+    h = utv.Handle(dev.index)
+    stream = h.stream
+
+    def step():
+        A.copy_(A0)
+        B.copy_(B0)
+        return h.lstsq(A, B, X, opts)
+
+    for _ in range(args.warmup):
+        r = step()
+    torch.cuda.synchronize()
+    rel_err = float(((X - X0).norm() / X0.norm()).item())
+
+    clocks = ClockSampler(dev.index)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    h.profile(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        r = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    prof = h.profile_read()
+    h.profile(False)
+    clk = clocks.stop()
+    t = e0.elapsed_time(e1) / 1e3 / args.steps
+    if world > 1:
+        tt = torch.tensor([t], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    F = f_alg(m, n, b, q, k, r)
+    value = world * F / t / 1e12
+
+    # ---- end-to-end through the C ABI with HOST buffers (H2D of A, B and D2H of X inside) ----
+    e2e = None
+    if not args.no_e2e:
+        Ah = utv.colmajor_empty(m, n, device="cpu", pin_memory=True)
+        Ah.copy_(A0)
+        Bh = utv.colmajor_empty(m, k, device="cpu", pin_memory=True)
+        Bh.copy_(B0)
+        Xh = utv.colmajor_empty(n, k, device="cpu", pin_memory=True)
+        h.lstsq(Ah, Bh, Xh, opts)                 # warm the staging buffers
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        re = h.lstsq(Ah, Bh, Xh, opts)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / 1e3
+        if world > 1:
+            tt = torch.tensor([te], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * F / te / 1e12, "unit": "TFLOP/s", "seconds": te,
+               "h2d_bytes_per_step": 8 * (m * n + m * k), "d2h_bytes_per_step": 8 * n * k, "steps": 1,
+               "rank_ok": re == r}
+        del Ah, Bh, Xh
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    peak, peak_src = fp64_peak()
+    g = prof["gemm"]
+    gemm_tf = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    total_ms = sum(v["ms"] for v in prof.values())
+    launches = int(sum(v["launches"] for v in prof.values()))
+    out = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "time_to_solution_s": t, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: square n={n} rank {r_true}, b={b}, q={q}, k={k} (paper generator "
+                               "P:2436-2448, known min-norm solution)", "m": m, "n": n, "rank": r_true, "block": b,
+                   "power_iters": q, "rhs": k, "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs (8mn = %.1f GB) >> 126 MB L2; no flush needed" % (8 * m * n / 1e9),
+                   "step": "restore A,B from a pristine device copy (D2D) + utv_lstsq"},
+        "frac_of_fp64_peak": value / (world * peak),
+        "fp64_peak_tflops": peak, "f_alg": F, "rank": r, "rank_ok": r == r_true, "rel_err_x0": rel_err,
+        "roofline": {"kernel": "dgemm_dmma_kernel (FP64 mma.sync DMMA, all GEMM launches of the step)",
+                     "bound": "tensor", "achieved": gemm_tf, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (gemm_tf / peak) if gemm_tf else None, "traffic": None,
+                     "peak_source": peak_src,
+                     "share_of_step": g["ms"] / (t * 1e3 * args.steps) if t > 0 else None},
+        "phases_ms_per_step": {k2: v["ms"] / args.steps for k2, v in prof.items()},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk,
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if not args.no_cpu_baseline and world >= 1 and rank == 0 and world == 1:
+        out["cpu_baseline"] = {k2: v for k2, v in cpu_baseline(args.cpu_n).items() if k2 != "seconds"}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=2048)
+    ap.add_argument("--ref-n", type=int, default=1536)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,124 @@
+/*
+ * utv.h -- C ABI of libutv.so: randUTV complete orthogonal decomposition and the
+ * fast-option least-squares solve of arXiv 2408.05238 (Chillaron, Quintana-Orti, Vidal,
+ * Martinsson), implemented as hand-written sm_100a (B200) CUDA kernels.
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source; readings R1..R18 are listed in
+ * DESIGN.md ("Readings of the paper").
+ *
+ * Conventions (all entry points):
+ *  - FP64, column-major, leading dimensions as in LAPACK (ld >= rows, ld >= 1).
+ *  - Matrix pointers are DEVICE pointers of the handle's device unless stated otherwise;
+ *    the caller allocates and owns every matrix.  The handle owns its workspace (allocated
+ *    lazily, reused, freed by utv_destroy).
+ *  - All work is enqueued on the handle's stream.  The only host synchronisation is the
+ *    device->host read of the numerical rank r in utv_factor / utv_lstsq.
+ *  - Errors are returned as utv_status, never by abort().  utv_last_error() gives a message.
+ *    Argument / shape errors are detected before anything is written; after a later
+ *    failure the contents of A, B, V, U and X are unspecified (LAPACK-like).
+ *  - One handle per host thread.
+ */
+#ifndef UTV_H_
+#define UTV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct utv_handle_s* utv_handle;
+
+typedef enum {
+  UTV_OK = 0,
+  UTV_ERR_ARG = -1,          /* bad argument (null pointer, ld < rows, b < 1, q < 0, tau not in [0,1)) */
+  UTV_ERR_SHAPE = -2,        /* m < n (the paper's loop guard for wide matrices is garbled: R4) */
+  UTV_ERR_ALLOC = -3,        /* device / pinned allocation failed */
+  UTV_ERR_CUDA = -4,         /* a CUDA runtime call failed */
+  UTV_ERR_NCCL = -5,         /* reserved: multi-GPU communication failure */
+  UTV_ERR_NUMERICAL = -6,    /* NaN/Inf in A or B, or the b x b Jacobi SVD exceeded 30 sweeps */
+  UTV_ERR_UNSUPPORTED = -7   /* a feature of this ABI that this build does not provide */
+} utv_status;
+
+enum {
+  UTV_WANT_V = 1u,           /* (informational: V is produced whenever a V pointer is passed) */
+  UTV_WANT_U = 2u,           /* build U explicitly (v21t semantics) when U != NULL */
+  UTV_NULLIFY_T12 = 4u,      /* reserved (NEXT): Nullify_top_right_part_of_T, fig:alg_nullify_t12 */
+  UTV_HOST_STREAMED = 8u     /* reserved (NEXT): out-of-core streaming from pinned host memory */
+};
+
+/* Parameters of randUTV(A, q, n_b) (fig:alg_utv) and Compute_rank. */
+typedef struct {
+  int64_t block;        /* n_b >= 1; this build supports n_b <= 256 (UTV_ERR_UNSUPPORTED above) */
+  int32_t power_iters;  /* q >= 0 ("q=1 or q=2 is sufficient") */
+  double tau;           /* rank tolerance in [0, 1): r = first j with T_jj <= tau * max_l T_ll (R10) */
+  uint64_t seed;        /* key of the Philox4x32-10 Gaussian sketch (R6) */
+  uint32_t flags;       /* UTV_WANT_* bits */
+} utv_opts;
+
+/* Create a handle bound to CUDA device `device`; `stream` is a cudaStream_t (NULL = the
+ * legacy default stream).  Returns UTV_ERR_CUDA if the device is unusable. */
+utv_status utv_create(utv_handle* handle, int device, void* stream);
+
+/* Multi-GPU handle (block-cyclic columns over NCCL).  Not provided by this
+ * build: returns UTV_ERR_UNSUPPORTED. */
+utv_status utv_create_dist(utv_handle* handle, int device, void* stream, const void* nccl_uid,
+                           int nranks, int rank);
+
+/* Release the handle and its workspace (synchronises its stream).  NULL is accepted. */
+utv_status utv_destroy(utv_handle handle);
+
+/* Message describing the last non-OK status on this handle ("" if none). */
+const char* utv_last_error(utv_handle handle);
+
+/* Change the stream of a handle (cudaStream_t). */
+utv_status utv_set_stream(utv_handle handle, void* stream);
+
+/* Wait for all work enqueued on the handle's stream. */
+utv_status utv_synchronize(utv_handle handle);
+
+/*
+ * randUTV: A V = U T (eq:UTVdef P:467-473), the blocked algorithm of fig:alg_utv
+ * with the readings R1 (the right update covers all rows), R3, R5, R13.
+ *   A (m x n, m >= n, lda >= m)  in: the matrix; out: T, upper trapezoidal, strictly-lower
+ *                                 part exactly 0, each n_b x n_b diagonal block diagonal with
+ *                                 non-negative, non-increasing entries (SVD of the block).
+ *   V (n x n, ldv >= n)           out if non-NULL: the orthogonal right factor.
+ *   U (m x m, ldu >= m)           out only if non-NULL and opts->flags & UTV_WANT_U.
+ *   B (m x k, ldb >= m)           if non-NULL and k > 0: overwritten by C = U^T B, applied on
+ *                                 the fly (v23t).
+ *   rank                          if non-NULL: r for opts->tau (R10); this reads r back to the
+ *                                 host (one synchronisation).
+ */
+utv_status utv_factor(utv_handle handle, int64_t m, int64_t n, double* A, int64_t lda, double* V,
+                      int64_t ldv, double* U, int64_t ldu, double* B, int64_t ldb, int64_t k,
+                      const utv_opts* opts, int64_t* rank);
+
+/*
+ * x_simple = V(:, 1:r) T11^{-1} U_1^T b (eq:simplesoln P:894-901), with C = U^T B from
+ * utv_factor:  X (n x k, ldx >= n) = V(:, 0:r) * T(0:r, 0:r)^{-1} * C(0:r, :).
+ * T (ldt >= m) is read-only (upper triangular in its leading r x r block); r == 0 -> X = 0.
+ */
+utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const double* T,
+                     int64_t ldt, const double* V, int64_t ldv, const double* C, int64_t ldc,
+                     int64_t k, double* X, int64_t ldx);
+
+/*
+ * Solve_linear_system, fast option (fig:alg_axb P:1075-1108 without the Nullify line;
+ * "Fast option" P:1114-1121; v34s): factor + Compute_rank + solve.  A and B are consumed
+ * (overwritten by T and U^T B); X (n x k) written; *rank = r.  V is kept in the handle's
+ * workspace.  A, B and X may be HOST pointers (pageable or pinned): they are then staged
+ * through device buffers inside the call (the end-to-end path).
+ */
+utv_status utv_lstsq(utv_handle handle, int64_t m, int64_t n, int64_t k, double* A, int64_t lda,
+                     double* B, int64_t ldb, double* X, int64_t ldx, const utv_opts* opts,
+                     int64_t* rank);
+
+/* Library version string, e.g. "utv-b200 0.1 sm_100a". */
+const char* utv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UTV_H_ */

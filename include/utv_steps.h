@@ -1,0 +1,81 @@
+/*
+ * utv_steps.h -- step-level entry points of libutv.so: each exposes one row of the hot
+ * path so that it can be checked against the oracle in isolation.
+ * Conventions as in utv.h (FP64, column-major, device pointers, the handle's stream,
+ * status returns, no host synchronisation unless stated).
+ */
+#ifndef UTV_STEPS_H_
+#define UTV_STEPS_H_
+
+#include "utv.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* a1 -- Gaussian sketch (reading R6).  G (mrows x b, ldg >= mrows):
+ * entry (i, c) = Box-Muller of Philox4x32-10 with key (lo32 seed, hi32 seed) and counter
+ * (lo32 g, hi32 g, c/2, step), g = row0 + i. */
+utv_status utv_sketch(utv_handle handle, uint64_t seed, int64_t step, int64_t row0, int64_t mrows,
+                      int64_t b, double* G, int64_t ldg);
+
+/* a1 (integer part) -- raw Philox4x32-10: out[4i..4i+3] = philox(ctr[4i..4i+3], key[2i..2i+1])
+ * for i < n (device arrays of uint32).  Bit-exact. */
+utv_status utv_philox(utv_handle handle, int64_t n, const uint32_t* ctr, const uint32_t* key,
+                      uint32_t* out);
+
+/* a3 / a5 -- Householder QR of P (m x w, m >= w, in place; R8):
+ * out P = R in the upper triangle, zeros strictly below; W (m x w, ldw >= m) the explicit
+ * unit-lower Householder vectors; tau (w); T (w x w, ldt >= w) upper triangular with
+ * H_0 ... H_{w-1} = I - W T W^T (LAPACK dlarfg/dlarft conventions). */
+utv_status utv_hqr(utv_handle handle, int64_t m, int64_t w, double* P, int64_t ldp, double* W,
+                   int64_t ldw, double* tau, double* T, int64_t ldt);
+
+/* a7 -- SVD of a b x b upper-triangular block (readings R9, R9b): one-sided
+ * Jacobi on R^T.  Out: U_s, V_s (b x b), sigma (b, non-negative, non-increasing) with
+ * R ~= U_s diag(sigma) V_s^T.  *sweeps (if non-NULL) gets the sweep count (synchronises).
+ * Requires 1 <= b <= 256.  UTV_ERR_NUMERICAL if Jacobi needed more than 30 sweeps. */
+utv_status utv_svd_small(utv_handle handle, int64_t b, const double* R, int64_t ldr, double* Us,
+                         int64_t ldu, double* sigma, double* Vs, int64_t ldv, int32_t* sweeps);
+
+/* a2 / a4 / a6 primitive -- FP64 DMMA GEMM: C = alpha op(A) op(B) + beta C, op = transpose
+ * when ta / tb != 0 (C is not read when beta == 0). */
+utv_status utv_gemm(utv_handle handle, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha,
+                    const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                    double* C, int64_t ldc);
+
+/* a8 -- Compute_rank (R10) of T's diagonal (n entries); synchronises. */
+utv_status utv_rank(utv_handle handle, int64_t n, const double* T, int64_t ldt, double tau,
+                    int64_t* rank);
+
+/* ---- instrumentation (bench.py) -----------------------------------------------------
+ * When enabled, every kernel launch of the library on this handle is bracketed by CUDA events
+ * on the handle's stream and tagged with a family; flops / bytes are the ALGORITHMIC counts of
+ * the launch (GEMM: 2MNK flops, 8(MK + KN + MN[+MN if beta != 0]) bytes). */
+enum {
+  UTV_PROF_GEMM = 0,    /* FP64 DMMA GEMM (+ its split-K reduce) */
+  UTV_PROF_PANEL = 1,   /* cooperative Householder sub-panel kernel */
+  UTV_PROF_SVD = 2,     /* Jacobi SVD kernels */
+  UTV_PROF_SKETCH = 3,  /* Philox sketch */
+  UTV_PROF_SOLVE = 4,   /* rank + block triangular solve */
+  UTV_PROF_MISC = 5,    /* copies, zeroing, identity, finiteness guard */
+  UTV_PROF_FAMILIES = 6
+};
+typedef struct {
+  int64_t launches;     /* kernel launches */
+  int64_t calls;        /* event-bracketed launch groups */
+  double ms;            /* sum of event-measured durations */
+  double flops;         /* algorithmic flops */
+  double bytes;         /* algorithmic bytes */
+} utv_prof_entry;
+
+/* enable != 0: start recording (clears previous records); 0: stop. */
+utv_status utv_profile(utv_handle handle, int enable);
+/* Fill out[0 .. UTV_PROF_FAMILIES-1] from the records so far (synchronises the stream). */
+utv_status utv_profile_read(utv_handle handle, utv_prof_entry* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UTV_STEPS_H_ */

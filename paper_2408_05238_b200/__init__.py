@@ -1,0 +1,291 @@
+"""paper_2408_05238_b200 -- B200-native randUTV + least squares (arXiv 2408.05238).
+
+Thin Python binding over the C ABI of ``libutv.so`` (``include/utv.h``, ``include/utv_steps.h``):
+argument marshalling only -- every step of the method runs in the sm_100a kernels of
+``csrc/``.  There is no CPU fallback: if ``libutv.so`` is missing or the device is not a
+CUDA GPU the calls raise.
+
+Matrices are column-major (LAPACK layout), passed as torch tensors of shape (rows, cols)
+with ``stride(0) == 1`` (e.g. ``colmajor(torch.empty(...))`` or ``t.t().contiguous().t()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libutv.so")
+
+UTV_OK, UTV_ERR_ARG, UTV_ERR_SHAPE, UTV_ERR_ALLOC, UTV_ERR_CUDA = 0, -1, -2, -3, -4
+UTV_ERR_NCCL, UTV_ERR_NUMERICAL, UTV_ERR_UNSUPPORTED = -5, -6, -7
+UTV_WANT_V, UTV_WANT_U, UTV_NULLIFY_T12, UTV_HOST_STREAMED = 1, 2, 4, 8
+
+EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "utv_set_stream", "utv_synchronize",
+            "utv_factor", "utv_solve", "utv_lstsq", "utv_version", "utv_sketch", "utv_philox", "utv_hqr",
+            "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read"]
+PROF_FAMILIES = ["gemm", "panel", "svd", "sketch", "solve", "misc"]
+
+
+class _ProfEntry(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("calls", C.c_int64), ("ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
+class UtvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libutv status {status}: {msg}")
+        self.status = status
+
+
+class _Opts(C.Structure):
+    _fields_ = [("block", C.c_int64), ("power_iters", C.c_int32), ("tau", C.c_double), ("seed", C.c_uint64),
+                ("flags", C.c_uint32)]
+
+
+@dataclass
+class Opts:
+    block: int = 256
+    power_iters: int = 2
+    tau: float = 1e-10
+    seed: int = 1
+    flags: int = 0
+
+    def c(self) -> _Opts:
+        return _Opts(int(self.block), int(self.power_iters), float(self.tau), int(self.seed), int(self.flags))
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libutv.so (raises if it has not been built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2408_05238_b200.build` "
+                               "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        p, i64, i32, u64, d = C.c_void_p, C.c_int64, C.c_int32, C.c_uint64, C.c_double
+        st = C.c_int
+        sig = {
+            "utv_create": ([C.POINTER(p), C.c_int, p], st),
+            "utv_create_dist": ([C.POINTER(p), C.c_int, p, p, C.c_int, C.c_int], st),
+            "utv_destroy": ([p], st),
+            "utv_last_error": ([p], C.c_char_p),
+            "utv_set_stream": ([p, p], st),
+            "utv_synchronize": ([p], st),
+            "utv_factor": ([p, i64, i64, p, i64, p, i64, p, i64, p, i64, i64, C.POINTER(_Opts), C.POINTER(i64)], st),
+            "utv_solve": ([p, i64, i64, i64, p, i64, p, i64, p, i64, i64, p, i64], st),
+            "utv_lstsq": ([p, i64, i64, i64, p, i64, p, i64, p, i64, C.POINTER(_Opts), C.POINTER(i64)], st),
+            "utv_version": ([], C.c_char_p),
+            "utv_sketch": ([p, u64, i64, i64, i64, i64, p, i64], st),
+            "utv_philox": ([p, i64, p, p, p], st),
+            "utv_hqr": ([p, i64, i64, p, i64, p, i64, p, p, i64], st),
+            "utv_svd_small": ([p, i64, p, i64, p, i64, p, p, i64, C.POINTER(i32)], st),
+            "utv_gemm": ([p, C.c_int, C.c_int, i64, i64, i64, d, p, i64, p, i64, d, p, i64], st),
+            "utv_rank": ([p, i64, p, i64, d, C.POINTER(i64)], st),
+            "utv_profile": ([p, C.c_int], st),
+            "utv_profile_read": ([p, p], st),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, res
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().utv_version().decode()
+
+
+# ----------------------------------------------------------------------------- layout helpers
+def colmajor_empty(rows: int, cols: int, device="cuda", dtype=torch.float64, pin_memory=False) -> torch.Tensor:
+    """An uninitialised column-major (rows x cols) tensor (storage = cols x rows row-major)."""
+    if str(device) == "cpu":
+        return torch.empty((cols, rows), dtype=dtype, pin_memory=pin_memory).t()
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def colmajor(t: torch.Tensor) -> torch.Tensor:
+    """Column-major copy (or the tensor itself if already column-major)."""
+    if t.dim() == 1:
+        t = t.reshape(-1, 1)
+    if t.stride(0) == 1 and (t.shape[1] <= 1 or t.stride(1) >= max(1, t.shape[0])):
+        return t
+    return t.t().contiguous().t()
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.dim() == 1:
+        return max(1, t.shape[0])
+    if t.stride(0) != 1 and t.shape[0] > 1:
+        raise ValueError("matrix must be column-major (stride(0) == 1); use colmajor()")
+    return max(1, t.shape[0], t.stride(1) if t.shape[1] > 1 else 0)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _check_f64(*ts):
+    for t in ts:
+        if t is not None and t.dtype != torch.float64:
+            raise TypeError("libutv computes in FP64: tensors must be torch.float64")
+
+
+class Handle:
+    """A libutv handle bound to one device and stream (default: torch's current stream)."""
+
+    def __init__(self, device: int | None = None, stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libutv needs a CUDA device (no CPU fallback)")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        self._check(lib().utv_create(C.byref(h), self.device, C.c_void_p(self.stream.cuda_stream)), None)
+        self.h = h
+
+    def _check(self, status: int, h):
+        if status != UTV_OK:
+            msg = lib().utv_last_error(h).decode() if h is not None else "utv_create failed"
+            raise UtvError(status, msg)
+
+    def check(self, status: int):
+        self._check(status, self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().utv_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def synchronize(self):
+        self.check(lib().utv_synchronize(self.h))
+
+    # ------------------------------------------------------------------ the boundary calls
+    def factor(self, A, V=None, U=None, B=None, opts: Opts | None = None, want_rank: bool = True):
+        """randUTV in place: A -> T; V, U (if given; U needs opts.flags & UTV_WANT_U), B -> U^T B."""
+        opts = opts or Opts()
+        _check_f64(A, V, U, B)
+        m, n = A.shape
+        k = 0 if B is None else (B.shape[1] if B.dim() == 2 else 1)
+        r = C.c_int64(-1)
+        o = opts.c()
+        self.check(lib().utv_factor(self.h, m, n, _ptr(A), _ld(A), _ptr(V), _ld(V) if V is not None else 1,
+                                    _ptr(U), _ld(U) if U is not None else 1, _ptr(B), _ld(B) if B is not None else 1,
+                                    k, C.byref(o), C.byref(r) if want_rank else None))
+        return int(r.value) if want_rank else None
+
+    def solve(self, T, V, Cm, r: int, X):
+        _check_f64(T, V, Cm, X)
+        m, n = T.shape
+        k = Cm.shape[1] if Cm.dim() == 2 else 1
+        self.check(lib().utv_solve(self.h, m, n, int(r), _ptr(T), _ld(T), _ptr(V), _ld(V), _ptr(Cm), _ld(Cm), k,
+                                   _ptr(X), _ld(X)))
+        return X
+
+    def lstsq(self, A, B, X, opts: Opts | None = None) -> int:
+        """Fast-option LS (A, B consumed).  A, B, X may be device or host tensors."""
+        opts = opts or Opts()
+        _check_f64(A, B, X)
+        m, n = A.shape
+        k = B.shape[1] if B.dim() == 2 else 1
+        r = C.c_int64(-1)
+        o = opts.c()
+        self.check(lib().utv_lstsq(self.h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(X), _ld(X), C.byref(o),
+                                   C.byref(r)))
+        return int(r.value)
+
+    # ------------------------------------------------------------------ step entry points
+    def sketch(self, seed: int, step: int, row0: int, mrows: int, b: int, G=None):
+        G = colmajor_empty(mrows, b, device=f"cuda:{self.device}") if G is None else G
+        self.check(lib().utv_sketch(self.h, seed, step, row0, mrows, b, _ptr(G), _ld(G)))
+        return G
+
+    def philox(self, ctr: torch.Tensor, key: torch.Tensor) -> torch.Tensor:
+        n = ctr.numel() // 4
+        out = torch.empty(4 * n, dtype=torch.int32, device=ctr.device)
+        self.check(lib().utv_philox(self.h, n, _ptr(ctr), _ptr(key), _ptr(out)))
+        return out
+
+    def hqr(self, P):
+        _check_f64(P)
+        m, w = P.shape
+        dev = P.device
+        W = colmajor_empty(m, w, device=dev)
+        tau = torch.empty(w, dtype=torch.float64, device=dev)
+        T = colmajor_empty(w, w, device=dev)
+        self.check(lib().utv_hqr(self.h, m, w, _ptr(P), _ld(P), _ptr(W), _ld(W), _ptr(tau), _ptr(T), _ld(T)))
+        return P, W, tau, T
+
+    def svd_small(self, R):
+        _check_f64(R)
+        b = R.shape[0]
+        dev = R.device
+        Us = colmajor_empty(b, b, device=dev); Vs = colmajor_empty(b, b, device=dev)
+        s = torch.empty(b, dtype=torch.float64, device=dev)
+        sw = C.c_int32(0)
+        self.check(lib().utv_svd_small(self.h, b, _ptr(R), _ld(R), _ptr(Us), _ld(Us), _ptr(s), _ptr(Vs), _ld(Vs),
+                                       C.byref(sw)))
+        return Us, s, Vs, int(sw.value)
+
+    def gemm(self, ta: bool, tb: bool, alpha: float, A, B, beta: float, Cm):
+        _check_f64(A, B, Cm)
+        M, N = Cm.shape
+        K = A.shape[0] if ta else A.shape[1]
+        self.check(lib().utv_gemm(self.h, int(ta), int(tb), M, N, K, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
+                                  float(beta), _ptr(Cm), _ld(Cm)))
+        return Cm
+
+    def profile(self, enable: bool):
+        self.check(lib().utv_profile(self.h, int(bool(enable))))
+
+    def profile_read(self) -> dict:
+        arr = (_ProfEntry * len(PROF_FAMILIES))()
+        self.check(lib().utv_profile_read(self.h, C.cast(arr, C.c_void_p)))
+        return {name: {"launches": e.launches, "calls": e.calls, "ms": e.ms, "flops": e.flops, "bytes": e.bytes}
+                for name, e in zip(PROF_FAMILIES, arr)}
+
+    def rank(self, T, tau: float) -> int:
+        r = C.c_int64(0)
+        n = T.shape[1]
+        self.check(lib().utv_rank(self.h, n, _ptr(T), _ld(T), float(tau), C.byref(r)))
+        return int(r.value)
+
+
+_default_handles: dict = {}
+
+
+def default_handle() -> Handle:
+    dev = torch.cuda.current_device()
+    h = _default_handles.get(dev)
+    if h is None:
+        h = _default_handles[dev] = Handle(dev)
+    return h
+
+
+def lstsq(A, B, opts: Opts | None = None, handle: Handle | None = None):
+    """x_simple for min ||A x - B|| (fast option).  Consumes (overwrites) A and B.
+
+    Returns (X, r) with X column-major (n x k) on the same device as A.
+    """
+    h = handle or default_handle()
+    m, n = A.shape
+    k = B.shape[1] if B.dim() == 2 else 1
+    X = colmajor_empty(n, k, device=A.device) if A.is_cuda else colmajor_empty(n, k, device="cpu")
+    r = h.lstsq(A, B if B.dim() == 2 else B.reshape(-1, 1), X, opts)
+    return X, r

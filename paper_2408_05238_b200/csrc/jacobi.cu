@@ -1,0 +1,224 @@
+// jacobi.cu -- a7: the small SVD of the b x b block R ("[A11, U_SVD, V_SVD] :=
+// SVD(A11)").  The paper leaves the method open; reading R9: one-sided Hestenes
+// Jacobi on W := R^T with rotations accumulated into U_s, pair skip tolerance sqrt(b) eps
+// (relative), numerically-zero columns (||w||^2 <= eps^2 ||R||_F^2, reading R9b) never rotated,
+// columns stably sorted by norm, then (V_s, R') := Householder QR of the sorted W with an
+// explicit Q, column signs flipped so R'_jj >= 0, sigma_j := R'_jj.
+//
+// B200 design: block one-sided Jacobi.  The b columns are split into 2P blocks of 16; a
+// cooperative grid of P CTAs (P = ceil(b/32), 8 at b = 256) runs a round-robin tournament over
+// the blocks (2P-1 rounds per sweep, one grid barrier per round).  In each round a CTA stages
+// its two blocks (32 columns of W and of J, 128 KiB at b = 256) in shared memory and runs a
+// full inner cyclic sweep over the 496 column pairs, 16 disjoint pairs at a time (one warp per
+// pair, 8 rows per lane, fixed-order warp reductions broadcast from lane 0).  The pair order
+// differs from the oracle's cyclic-by-rows order, so sigma agrees to rounding and U_s / V_s
+// agree up to rotations inside clusters of equal singular values (x is invariant).
+#include "kernels.cuh"
+#include "prof.cuh"
+
+namespace utv {
+
+namespace {
+constexpr int JBLK = 16;
+constexpr int JT = 512;
+
+__device__ __forceinline__ double warp_sum_bcast(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+__global__ void __launch_bounds__(JT, 1)
+jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const double* __restrict__ fro2, double tol,
+              int max_sweeps, int* __restrict__ rot, int* __restrict__ info, unsigned* __restrict__ bar) {
+  extern __shared__ __align__(16) double jsm[];
+  double* sW = jsm;
+  double* sJ = jsm + 2 * JBLK * bw;
+  __shared__ int s_gcol[2 * JBLK];
+  __shared__ int s_rot;
+  __shared__ int s_done;
+  __shared__ unsigned s_gen;
+  const int P = gridDim.x, nblk = 2 * P, c = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_gen = *((volatile unsigned*)bar + 1);
+  __syncthreads();
+  unsigned gen = s_gen;
+  const double eps = 0x1.0p-52;
+  const double small2 = eps * eps * fro2[0];   // R9b: numerically-zero column floor
+
+  int sweep = 0;
+  bool converged = false;
+  for (sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int r = 0; r < nblk - 1; ++r) {
+      const int bp = (c == 0) ? 0 : 1 + (c - 1 + r) % (nblk - 1);
+      const int kq = nblk - 1 - c;
+      const int bq = (kq == 0) ? 0 : 1 + (kq - 1 + r) % (nblk - 1);
+      if (tid < 2 * JBLK) s_gcol[tid] = tid < JBLK ? bp * JBLK + tid : bq * JBLK + (tid - JBLK);
+      if (tid == 0) s_rot = 0;
+      __syncthreads();
+      for (int e = tid; e < 2 * JBLK * bw; e += JT) {
+        const int col = e / bw, row = e % bw, gc = s_gcol[col];
+        sW[e] = gc < bw ? __ldcg(W + (size_t)gc * bw + row) : 0.0;
+        sJ[e] = gc < bw ? __ldcg(J + (size_t)gc * bw + row) : 0.0;
+      }
+      __syncthreads();
+      for (int ir = 0; ir < 2 * JBLK - 1; ++ir) {
+        if (warp < JBLK) {
+          int a = (warp == 0) ? 0 : 1 + (warp - 1 + ir) % (2 * JBLK - 1);
+          const int kb = 2 * JBLK - 1 - warp;
+          int b = (kb == 0) ? 0 : 1 + (kb - 1 + ir) % (2 * JBLK - 1);
+          int ga = s_gcol[a], gb = s_gcol[b];
+          if (ga > gb) { int t0 = a; a = b; b = t0; t0 = ga; ga = gb; gb = t0; }
+          if (gb < bw) {
+            double* wi = sW + a * bw;
+            double* wj = sW + b * bw;
+            double al = 0.0, be = 0.0, gm = 0.0;
+            for (int row = lane; row < bw; row += 32) {
+              const double x = wi[row], y = wj[row];
+              al += x * x; be += y * y; gm += x * y;
+            }
+            al = warp_sum_bcast(al); be = warp_sum_bcast(be); gm = warp_sum_bcast(gm);
+            const bool skip = (gm == 0.0) || al <= small2 || be <= small2 || fabs(gm) <= tol * sqrt(al) * sqrt(be);
+            if (!skip) {
+              const double zeta = (be - al) / (2.0 * gm);
+              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              const double cs = 1.0 / sqrt(1.0 + t * t);
+              const double sn = cs * t;
+              double* ji = sJ + a * bw;
+              double* jj = sJ + b * bw;
+              for (int row = lane; row < bw; row += 32) {
+                const double x = wi[row], y = wj[row];
+                wi[row] = cs * x - sn * y;
+                wj[row] = sn * x + cs * y;
+                const double u = ji[row], v = jj[row];
+                ji[row] = cs * u - sn * v;
+                jj[row] = sn * u + cs * v;
+              }
+              if (lane == 0) atomicAdd(&s_rot, 1);
+            }
+          }
+        }
+        __syncthreads();
+      }
+      for (int e = tid; e < 2 * JBLK * bw; e += JT) {
+        const int col = e / bw, row = e % bw, gc = s_gcol[col];
+        if (gc < bw) {
+          __stcg(W + (size_t)gc * bw + row, sW[e]);
+          __stcg(J + (size_t)gc * bw + row, sJ[e]);
+        }
+      }
+      if (tid == 0 && s_rot) atomicAdd(rot + sweep, s_rot);
+      grid_sync(bar, P, gen);
+    }
+    if (tid == 0) s_done = (atomicAdd(rot + sweep, 0) == 0);
+    __syncthreads();
+    if (s_done) { converged = true; break; }
+  }
+  if (c == 0 && tid == 0) {   // accumulated over the steps of one factorization
+    atomicMax(info, converged ? sweep + 1 : sweep);
+    if (!converged) atomicOr(info + 1, 1);
+  }
+}
+
+// ||R||_F^2 of W (= R^T), fixed-order; one CTA.
+__global__ void fro2_kernel(int bw, const double* __restrict__ W, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int e = threadIdx.x; e < bw * bw; e += blockDim.x) s += W[e] * W[e];
+  s = warp_sum_bcast(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) t += red[w];
+    out[0] = t;
+  }
+}
+
+// W := R^T, J := I
+__global__ void jacobi_init_kernel(int bw, const double* __restrict__ R, int64_t ldr, double* __restrict__ W,
+                                   double* __restrict__ J) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bw * bw; e += gridDim.x * blockDim.x) {
+    const int i = e % bw, j = e / bw;
+    W[e] = R[cm(j, i, ldr)];
+    J[e] = i == j ? 1.0 : 0.0;
+  }
+}
+
+// stable sort of the columns by norm (descending): Ws = W P, Us = J P
+__global__ void jacobi_sort_kernel(int bw, const double* __restrict__ W, const double* __restrict__ J,
+                                   double* __restrict__ Ws, double* __restrict__ Us, int64_t ldu) {
+  __shared__ double nrm[256];
+  __shared__ int pos[256];
+  for (int j = threadIdx.x; j < bw; j += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < bw; ++r) s += W[(size_t)j * bw + r] * W[(size_t)j * bw + r];
+    nrm[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < bw; j += blockDim.x) {
+    int p = 0;
+    for (int l = 0; l < bw; ++l) p += (nrm[l] > nrm[j]) || (nrm[l] == nrm[j] && l < j);
+    pos[j] = p;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < bw * bw; e += blockDim.x) {
+    const int r = e % bw, j = e / bw, p = pos[j];
+    Ws[(size_t)p * bw + r] = W[e];
+    Us[cm(r, p, ldu)] = J[e];
+  }
+}
+
+// V_s[:, j] = sgn_j (e_j - Q[:, j]), sigma_j = |R'_jj|
+__global__ void jacobi_vs_kernel(int bw, const double* __restrict__ Q, const double* __restrict__ Rp,
+                                 double* __restrict__ Vs, int64_t ldv, double* __restrict__ sigma) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bw * bw; e += gridDim.x * blockDim.x) {
+    const int r = e % bw, j = e / bw;
+    const double d = Rp[(size_t)j * bw + j];
+    const double v = (r == j ? 1.0 : 0.0) - Q[e];
+    Vs[cm(r, j, ldv)] = d < 0.0 ? -v : v;
+    if (r == 0) sigma[j] = fabs(d);
+  }
+}
+}  // namespace
+
+void svd_small(cudaStream_t st, int64_t bw64, const double* R, int64_t ldr, double* Us, int64_t ldu, double* sigma,
+               double* Vs, int64_t ldv, const SvdWork& sw) {
+  const int bw = (int)bw64;
+  if (bw <= 0) return;
+  {
+  ProfScope prof_a(st, kProfSvd, 4, 0.0, 0.0);
+  jacobi_init_kernel<<<std::max(1, std::min(bw * bw / 256, 256)), 256, 0, st>>>(bw, R, ldr, sw.W, sw.J);
+  UTV_CUDA(cudaGetLastError());
+  fro2_kernel<<<1, 1024, 0, st>>>(bw, sw.W, sw.X);   // X[0] = ||R||_F^2 (scratch)
+  UTV_CUDA(cudaGetLastError());
+  UTV_CUDA(cudaMemsetAsync(sw.rot, 0, sizeof(int) * kMaxSweeps, st));
+  static bool attr = false;
+  if (!attr) {
+    UTV_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  4 * JBLK * 256 * (int)sizeof(double)));
+    attr = true;
+  }
+  int P = (bw + 2 * JBLK - 1) / (2 * JBLK);
+  size_t smem = (size_t)4 * JBLK * bw * sizeof(double);
+  int bwv = bw;
+  const double* fro2 = sw.X;
+  double tol = sqrt((double)bw) * 0x1.0p-52;
+  int maxs = kMaxSweeps;
+  void* args[] = {&bwv, (void*)&sw.W, (void*)&sw.J, &fro2, &tol, &maxs, (void*)&sw.rot, (void*)&sw.info,
+                  (void*)&sw.pw.bar};
+  UTV_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_kernel, dim3(P), dim3(JT), args, smem, st));
+  jacobi_sort_kernel<<<1, 256, 0, st>>>(bw, sw.W, sw.J, sw.Ws, Us, ldu);
+  UTV_CUDA(cudaGetLastError());
+  }
+  panel_qr(st, bw, bw, sw.Ws, bw, sw.Wh, bw, sw.tau, sw.Tq, bw, sw.pw);
+  dgemm(st, false, true, bw, bw, bw, 1.0, sw.Tq, bw, sw.Wh, bw, 0.0, sw.X, bw, sw.pw.gemm_work,
+        sw.pw.gemm_work_doubles, sw.pw.num_sms);
+  dgemm(st, false, false, bw, bw, bw, 1.0, sw.Wh, bw, sw.X, bw, 0.0, sw.Q, bw, sw.pw.gemm_work,
+        sw.pw.gemm_work_doubles, sw.pw.num_sms);
+  ProfScope prof_b(st, kProfSvd, 1, 0.0, 0.0);
+  jacobi_vs_kernel<<<std::max(1, std::min(bw * bw / 256, 256)), 256, 0, st>>>(bw, sw.Q, sw.Ws, Vs, ldv, sigma);
+  UTV_CUDA(cudaGetLastError());
+}
+
+}  // namespace utv

@@ -1,0 +1,66 @@
+// kernels.cuh -- launchers of the sm_100a randUTV kernels (internal to libutv.so).
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace utv {
+
+// ---- a1: Philox4x32-10 Gaussian sketch (sketch.cu) --------------------------------------
+void launch_sketch(cudaStream_t st, uint64_t seed, int64_t step, int64_t row0, int64_t mrows, int64_t b, double* G,
+                   int64_t ldg, int num_sms);
+void launch_philox_words(cudaStream_t st, const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out);
+
+// ---- a3/a5: Householder panel QR (panel_qr.cu) -------------------------------------------
+struct PanelWork {
+  double* part;          // >= num_sms * 32 doubles (per-CTA partial sums)
+  double* z1;            // >= 32 * w doubles
+  double* z2;            // >= 32 * w doubles
+  double* gram;          // >= w * w doubles
+  double* x;             // >= w * 32 doubles
+  double* gemm_work;     // split-K workspace
+  size_t gemm_work_doubles;
+  unsigned* bar;         // 2 unsigned, bar[0] == 0 between launches
+  int num_sms;
+};
+// In place: P (rows x w) -> R (upper triangle), zeros strictly below; W (rows x w) the explicit
+// unit-lower Householder vectors; tau (w); T (w x w, upper, zeros below) with
+// Q = H_0 ... H_{w-1} = I - W T W^T.  Requires rows >= w.
+void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
+              double* T, int64_t ldt, const PanelWork& pw);
+
+// ---- a7: small SVD (jacobi.cu) -----------------------------------------------------------
+struct SvdWork {
+  double* W;      // bw * bw
+  double* J;      // bw * bw
+  double* Ws;     // bw * bw
+  double* Wh;     // bw * bw
+  double* Tq;     // bw * bw
+  double* X;      // bw * bw
+  double* Q;      // bw * bw
+  double* tau;    // bw
+  int* rot;       // kMaxSweeps ints
+  int* info;      // 2 ints: sweeps, status
+  PanelWork pw;
+};
+constexpr int kMaxSweeps = 30;
+// R (bw x bw upper triangular, ldr) -> U_s, sigma, V_s with R ~= U_s diag(sigma) V_s^T.
+// Asynchronous; info[1] != 0 flags non-convergence (checked by the caller).
+void svd_small(cudaStream_t st, int64_t bw, const double* R, int64_t ldr, double* Us, int64_t ldu, double* sigma,
+               double* Vs, int64_t ldv, const SvdWork& sw);
+
+// ---- a8/a9: rank and solve (solve.cu) ----------------------------------------------------
+void launch_rank(cudaStream_t st, int64_t n, const double* T, int64_t ldt, double tau, int64_t* r_dev);
+// In place z := T(j0:j1, j0:j1)^{-1} z for the rows j0..j1-1 of Z (ldz), k columns.
+void launch_trsv_block(cudaStream_t st, int64_t j0, int64_t j1, const double* T, int64_t ldt, double* Z, int64_t ldz,
+                       int64_t k);
+
+// ---- misc (misc.cu) ----------------------------------------------------------------------
+void launch_set_identity(cudaStream_t st, int64_t rows, int64_t cols, double* A, int64_t lda);
+void launch_set_zero(cudaStream_t st, int64_t rows, int64_t cols, double* A, int64_t lda);
+void launch_set_diag(cudaStream_t st, int64_t bw, const double* sigma, double* A, int64_t lda);
+void launch_copy(cudaStream_t st, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd);
+void launch_zero_strict_lower(cudaStream_t st, int64_t rows, int64_t cols, double* A, int64_t lda);
+// flag[0] |= any non-finite entry in A (rows x cols)
+void launch_check_finite(cudaStream_t st, int64_t rows, int64_t cols, const double* A, int64_t lda, int* flag);
+
+}  // namespace utv

@@ -1,0 +1,89 @@
+// solve.cu -- a8 Compute_rank (reading R10: relative to max_l T_ll,
+// prefix rule) and the block triangular solve of a9, x_simple = V(:,1:r) T11^{-1} U_1^T b
+// (eq:simplesoln P:894-901).  The large parts of a9 (the updates above each diagonal block and
+// X = V(:, 0:r) z) are DMMA GEMMs; these kernels are the latency-bound pieces.
+#include "kernels.cuh"
+#include "prof.cuh"
+
+namespace utv {
+
+namespace {
+__global__ void rank_kernel(int64_t n, const double* __restrict__ T, int64_t ldt, double tau, int64_t* r_out) {
+  __shared__ double smax[32];
+  __shared__ long long sidx[32];
+  __shared__ double s_dmax;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double m = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) m = fmax(m, T[cm(j, j, ldt)]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) smax[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = 0.0;
+    for (int w = 0; w < nw; ++w) d = fmax(d, smax[w]);
+    s_dmax = d;
+  }
+  __syncthreads();
+  const double dmax = s_dmax;
+  long long first = (long long)n;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
+    if (T[cm(j, j, ldt)] <= tau * dmax) { first = (long long)j; break; }
+  for (int o = 16; o > 0; o >>= 1) {
+    long long other = __shfl_xor_sync(0xffffffffu, first, o);
+    first = other < first ? other : first;
+  }
+  if (lane == 0) sidx[warp] = first;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long f = (long long)n;
+    for (int w = 0; w < nw; ++w) f = sidx[w] < f ? sidx[w] : f;
+    *r_out = (dmax == 0.0) ? 0 : (int64_t)f;
+  }
+}
+
+// Column-oriented back substitution on one diagonal block (<= 256 rows), k RHS in chunks of 16.
+constexpr int TS_ROWS = 256, TS_K = 16;
+__global__ void trsv_block_kernel(int64_t j0, int64_t j1, const double* __restrict__ T, int64_t ldt,
+                                  double* __restrict__ Z, int64_t ldz, int64_t k) {
+  __shared__ double z[TS_K][TS_ROWS];
+  const int bs = (int)(j1 - j0);
+  for (int64_t c0 = 0; c0 < k; c0 += TS_K) {
+    const int kc = (int)((k - c0) < TS_K ? (k - c0) : TS_K);
+    for (int e = threadIdx.x; e < bs * kc; e += blockDim.x) {
+      const int p = e % bs, c = e / bs;
+      z[c][p] = Z[cm(j0 + p, c0 + c, ldz)];
+    }
+    __syncthreads();
+    for (int i = bs - 1; i >= 0; --i) {
+      if (threadIdx.x < kc) z[threadIdx.x][i] /= T[cm(j0 + i, j0 + i, ldt)];
+      __syncthreads();
+      for (int e = threadIdx.x; e < i * kc; e += blockDim.x) {
+        const int p = e % i, c = e / i;
+        z[c][p] -= T[cm(j0 + p, j0 + i, ldt)] * z[c][i];
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < bs * kc; e += blockDim.x) {
+      const int p = e % bs, c = e / bs;
+      Z[cm(j0 + p, c0 + c, ldz)] = z[c][p];
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+void launch_rank(cudaStream_t st, int64_t n, const double* T, int64_t ldt, double tau, int64_t* r_dev) {
+  ProfScope prof(st, kProfSolve, 1, 0.0, 8.0 * (double)n);
+  rank_kernel<<<1, 1024, 0, st>>>(n, T, ldt, tau, r_dev);
+  UTV_CUDA(cudaGetLastError());
+}
+
+void launch_trsv_block(cudaStream_t st, int64_t j0, int64_t j1, const double* T, int64_t ldt, double* Z, int64_t ldz,
+                       int64_t k) {
+  if (j1 <= j0 || k <= 0) return;
+  ProfScope prof(st, kProfSolve, 1, (double)(j1 - j0) * (j1 - j0) * k, 8.0 * (j1 - j0) * (j1 - j0) / 2);
+  trsv_block_kernel<<<1, 256, 0, st>>>(j0, j1, T, ldt, Z, ldz, k);
+  UTV_CUDA(cudaGetLastError());
+}
+
+}  // namespace utv

@@ -1,0 +1,549 @@
+// utv_api.cu -- the C ABI of libutv.so (include/utv.h, include/utv_steps.h) and the host
+// orchestration of randUTV on one B200: the per-step launch sequence of fig:alg_utv
+// over the sm_100a kernels, the handle's workspace arena and error mapping.
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/utv.h"
+#include "../../include/utv_steps.h"
+#include "kernels.cuh"
+#include "prof.cuh"
+
+using namespace utv;
+
+struct utv_handle_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = kNumSMsDefault;
+  std::string last_error;
+  // workspace arena (device)
+  double* ws = nullptr;
+  size_t ws_doubles = 0;
+  unsigned* bar = nullptr;       // grid-barrier state: [0] count, [1] generation
+  int* info = nullptr;           // Jacobi sweeps / failure flag
+  int* flag = nullptr;           // finiteness flag
+  int64_t* d_rank = nullptr;
+  int64_t* h_rank = nullptr;     // pinned
+  int* h_info = nullptr;         // pinned (info[0..1], flag)
+  // lstsq buffers
+  double* vbuf = nullptr; size_t vbuf_doubles = 0;
+  double* stage = nullptr; size_t stage_doubles = 0;   // host-pointer staging (A, B, X)
+  Profiler prof;
+};
+
+namespace {
+
+struct ApiError {
+  utv_status st;
+  std::string msg;
+};
+
+void fail(utv_status st, const std::string& m) { throw ApiError{st, m}; }
+
+template <typename F>
+utv_status guarded(utv_handle h, F&& f) {
+  if (!h) return UTV_ERR_ARG;
+  try {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != h->device) UTV_CUDA(cudaSetDevice(h->device));
+    struct ProfBind {
+      explicit ProfBind(Profiler* p) { g_prof = p; }
+      ~ProfBind() { g_prof = nullptr; }
+    } bind(h->prof.on ? &h->prof : nullptr);
+    f();
+    h->last_error.clear();
+    return UTV_OK;
+  } catch (const ApiError& e) {
+    h->last_error = e.msg;
+    return e.st;
+  } catch (const CudaError& e) {
+    h->last_error = std::string("CUDA error '") + cudaGetErrorString(e.err) + "' in " + e.what + " (utv_api/kernels line " +
+                    std::to_string(e.line) + ")";
+    cudaGetLastError();
+    return e.err == cudaErrorMemoryAllocation ? UTV_ERR_ALLOC : UTV_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    h->last_error = "host allocation failed";
+    return UTV_ERR_ALLOC;
+  }
+}
+
+void ensure_buf(double** p, size_t* have, size_t need) {
+  if (*have >= need) return;
+  if (*p) { UTV_CUDA(cudaFree(*p)); *p = nullptr; *have = 0; }
+  cudaError_t e = cudaMalloc((void**)p, need * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    fail(UTV_ERR_ALLOC, "device allocation of " + std::to_string(need * sizeof(double)) + " bytes failed");
+  }
+  *have = need;
+}
+
+// Workspace layout for one factorization (offsets in doubles).
+struct Layout {
+  size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, Tu, tauu, Z1, Z2, tmp, R, Us, Vs, sig;
+  size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve;
+  size_t gemm_doubles;
+  size_t total;
+};
+
+Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t cnt) { size_t o = off; off += (cnt + 31) / 32 * 32; return o; };
+  const size_t mx = (size_t)std::max(m, n);
+  const size_t nk = (size_t)std::max<int64_t>(n, std::max<int64_t>(k, 1));
+  L.G = take((size_t)m * b);
+  L.Y = take((size_t)n * b);
+  L.Z = take((size_t)m * b);
+  L.Wv = take((size_t)n * b);
+  L.Tv = take((size_t)b * b);
+  L.tauv = take(b);
+  L.X = take(mx * b);
+  L.X2 = take(mx * b);
+  L.Wu = take((size_t)m * b);
+  L.Tu = take((size_t)b * b);
+  L.tauu = take(b);
+  L.Z1 = take((size_t)b * nk);
+  L.Z2 = take((size_t)b * nk);
+  L.tmp = take(std::max<size_t>(mx * b, (size_t)b * nk));
+  L.R = take((size_t)b * b);
+  L.Us = take((size_t)b * b);
+  L.Vs = take((size_t)b * b);
+  L.sig = take(b);
+  L.sW = take((size_t)b * b);
+  L.sJ = take((size_t)b * b);
+  L.sWs = take((size_t)b * b);
+  L.sWh = take((size_t)b * b);
+  L.sTq = take((size_t)b * b);
+  L.sX = take((size_t)b * b);
+  L.sQ = take((size_t)b * b);
+  L.stau = take(b);
+  L.part = take((size_t)num_sms * 32);
+  L.pz1 = take((size_t)32 * b);
+  L.pz2 = take((size_t)32 * b);
+  L.gram = take((size_t)b * b);
+  L.px = take((size_t)b * 32);
+  L.zsolve = take((size_t)n * std::max<int64_t>(k, 1));
+  L.gemm_doubles = std::max<size_t>((size_t)128 * b * std::max<int64_t>(b, 32), (size_t)1 << 22);
+  L.gemm = take(L.gemm_doubles);
+  L.total = off;
+  return L;
+}
+
+struct Ctx {
+  utv_handle h;
+  cudaStream_t st;
+  Layout L;
+  double* w;
+  PanelWork pw;
+  SvdWork sw;
+  double* at(size_t off) const { return w + off; }
+  void gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+            const double* B, int64_t ldb, double beta, double* C, int64_t ldc) const {
+    dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, at(L.gemm), L.gemm_doubles, h->num_sms);
+  }
+};
+
+Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
+  Ctx c;
+  c.h = h;
+  c.st = h->stream;
+  c.L = plan(m, n, k, b, h->num_sms);
+  ensure_buf(&h->ws, &h->ws_doubles, c.L.total);
+  c.w = h->ws;
+  const Layout& L = c.L;
+  c.pw = PanelWork{c.at(L.part), c.at(L.pz1), c.at(L.pz2), c.at(L.gram), c.at(L.px), c.at(L.gemm), L.gemm_doubles,
+                   h->bar, h->num_sms};
+  c.sw = SvdWork{c.at(L.sW), c.at(L.sJ), c.at(L.sWs), c.at(L.sWh), c.at(L.sTq), c.at(L.sX), c.at(L.sQ), c.at(L.stau),
+                 h->info + 2, h->info, c.pw};
+  return c;
+}
+
+void check_opts(const utv_opts* o) {
+  if (!o) fail(UTV_ERR_ARG, "opts is NULL");
+  if (o->block < 1) fail(UTV_ERR_ARG, "opts->block < 1");
+  if (o->block > 256) fail(UTV_ERR_UNSUPPORTED, "opts->block > 256 is not supported by this build");
+  if (o->power_iters < 0) fail(UTV_ERR_ARG, "opts->power_iters < 0");
+  if (!(o->tau >= 0.0 && o->tau < 1.0)) fail(UTV_ERR_ARG, "opts->tau not in [0, 1)");
+}
+
+void check_ld(const char* name, int64_t ld, int64_t rows) {
+  if (ld < std::max<int64_t>(1, rows)) fail(UTV_ERR_ARG, std::string(name) + " < max(1, rows)");
+}
+
+// Copy a (rows x cols) column-major matrix between (possibly host) buffers on the stream.
+void copy2d(cudaStream_t st, void* dst, int64_t ldd, const void* src, int64_t lds, int64_t rows, int64_t cols,
+            cudaMemcpyKind kind) {
+  if (rows <= 0 || cols <= 0) return;
+  UTV_CUDA(cudaMemcpy2DAsync(dst, (size_t)ldd * 8, src, (size_t)lds * 8, (size_t)rows * 8, (size_t)cols, kind, st));
+}
+
+// The randUTV factorization on device buffers (fig:alg_utv).
+void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, double* V, int64_t ldv, double* U,
+                 int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts& o) {
+  cudaStream_t st = c.st;
+  const Layout& L = c.L;
+  const int64_t b = o.block;
+  const int ns = c.h->num_sms;
+  UTV_CUDA(cudaMemsetAsync(c.h->info, 0, 4 * sizeof(int), st));
+  UTV_CUDA(cudaMemsetAsync(c.h->flag, 0, sizeof(int), st));
+  launch_check_finite(st, m, n, A, lda, c.h->flag);
+  if (B && k > 0) launch_check_finite(st, m, k, B, ldb, c.h->flag);
+  if (V) launch_set_identity(st, n, n, V, ldv);
+  if (U) launch_set_identity(st, m, m, U, ldu);
+  double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *Wv = c.at(L.Wv), *Tv = c.at(L.Tv), *tauv = c.at(L.tauv);
+  double *X = c.at(L.X), *X2 = c.at(L.X2), *Wu = c.at(L.Wu), *Tu = c.at(L.Tu), *tauu = c.at(L.tauu);
+  double *Z1 = c.at(L.Z1), *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp), *Us = c.at(L.Us), *Vs = c.at(L.Vs),
+         *sig = c.at(L.sig);
+
+  for (int64_t j0 = 0, step = 0; j0 < n; j0 += b, ++step) {
+    const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0, nr = np - bw;
+    double* Ap = A + cm(j0, j0, lda);
+    // ---- apply transformations from the right ----
+    if (np > b) {  // R5: no sketch for the last block
+      launch_sketch(st, o.seed, step, j0, mp, b, G, mp, ns);                          // a1
+      c.gemm(true, false, np, b, mp, 1.0, Ap, lda, G, mp, 0.0, Y, np);                // Y = A'^T G
+      for (int32_t it = 0; it < o.power_iters; ++it) {                                // a2 (R7)
+        c.gemm(false, false, mp, b, np, 1.0, Ap, lda, Y, np, 0.0, Z, mp);             // Z = A' Y
+        c.gemm(true, false, np, b, mp, 1.0, Ap, lda, Z, mp, 0.0, Y, np);              // Y = A'^T Z
+      }
+      panel_qr(st, np, b, Y, np, Wv, np, tauv, Tv, b, c.pw);                          // a3
+      double* Ac = A + cm(0, j0, lda);                                                 // a4, R1: all rows
+      c.gemm(false, false, m, b, np, 1.0, Ac, lda, Wv, np, 0.0, X, m);
+      c.gemm(false, false, m, b, b, 1.0, X, m, Tv, b, 0.0, X2, m);
+      c.gemm(false, true, m, np, b, -1.0, X2, m, Wv, np, 1.0, Ac, lda);
+      if (V) {
+        double* Vc = V + cm(0, j0, ldv);
+        c.gemm(false, false, n, b, np, 1.0, Vc, ldv, Wv, np, 0.0, X, n);
+        c.gemm(false, false, n, b, b, 1.0, X, n, Tv, b, 0.0, X2, n);
+        c.gemm(false, true, n, np, b, -1.0, X2, n, Wv, np, 1.0, Vc, ldv);
+      }
+    }
+    // ---- apply transformations from the left ----
+    panel_qr(st, mp, bw, Ap, lda, Wu, mp, tauu, Tu, b, c.pw);                           // a5 (+R13)
+    if (nr > 0) {                                                                       // a6, R3
+      double* Ar = A + cm(j0, j0 + bw, lda);
+      c.gemm(true, false, bw, nr, mp, 1.0, Wu, mp, Ar, lda, 0.0, Z1, bw);
+      c.gemm(true, false, bw, nr, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+      c.gemm(false, false, mp, nr, bw, -1.0, Wu, mp, Z2, bw, 1.0, Ar, lda);
+    }
+    if (B && k > 0) {                                                                   // C := Q_U^T C (v23t)
+      double* Cr = B + cm(j0, 0, ldb);
+      c.gemm(true, false, bw, k, mp, 1.0, Wu, mp, Cr, ldb, 0.0, Z1, bw);
+      c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+      c.gemm(false, false, mp, k, bw, -1.0, Wu, mp, Z2, bw, 1.0, Cr, ldb);
+    }
+    if (U) {
+      double* Uc = U + cm(0, j0, ldu);
+      c.gemm(false, false, m, bw, mp, 1.0, Uc, ldu, Wu, mp, 0.0, X, m);
+      c.gemm(false, false, m, bw, bw, 1.0, X, m, Tu, b, 0.0, X2, m);
+      c.gemm(false, true, m, mp, bw, -1.0, X2, m, Wu, mp, 1.0, Uc, ldu);
+    }
+    // ---- small SVD and the four updates ----
+    svd_small(st, bw, Ap, lda, Us, b, sig, Vs, b, c.sw);                               // a7
+    launch_set_diag(st, bw, sig, Ap, lda);
+    if (j0 > 0) {                                                                       // A01 := A01 V_s
+      double* A01 = A + cm(0, j0, lda);
+      c.gemm(false, false, j0, bw, bw, 1.0, A01, lda, Vs, b, 0.0, tmp, j0);
+      launch_copy(st, j0, bw, tmp, j0, A01, lda);
+    }
+    if (nr > 0) {                                                                       // A12 := U_s^T A12
+      double* A12 = A + cm(j0, j0 + bw, lda);
+      c.gemm(true, false, bw, nr, bw, 1.0, Us, b, A12, lda, 0.0, tmp, bw);
+      launch_copy(st, bw, nr, tmp, bw, A12, lda);
+    }
+    if (V) {                                                                            // V1 := V1 V_s
+      double* V1 = V + cm(0, j0, ldv);
+      c.gemm(false, false, n, bw, bw, 1.0, V1, ldv, Vs, b, 0.0, tmp, n);
+      launch_copy(st, n, bw, tmp, n, V1, ldv);
+    }
+    if (B && k > 0) {                                                                   // C1 := U_s^T C1
+      double* C1 = B + cm(j0, 0, ldb);
+      c.gemm(true, false, bw, k, bw, 1.0, Us, b, C1, ldb, 0.0, tmp, bw);
+      launch_copy(st, bw, k, tmp, bw, C1, ldb);
+    }
+    if (U) {                                                                            // U1 := U1 U_s
+      double* U1 = U + cm(0, j0, ldu);
+      c.gemm(false, false, m, bw, bw, 1.0, U1, ldu, Us, b, 0.0, tmp, m);
+      launch_copy(st, m, bw, tmp, m, U1, ldu);
+    }
+  }
+  if (m > n) launch_set_zero(st, m - n, n, A + n, lda);   // rows below T (already 0 by R13; kept explicit)
+}
+
+// Reads back the Jacobi / finiteness flags and the rank (one synchronisation).
+int64_t finish_factor(const Ctx& c, int64_t n, const double* T, int64_t ldt, double tau, bool want_rank) {
+  cudaStream_t st = c.st;
+  if (want_rank) {
+    launch_rank(st, n, T, ldt, tau, c.h->d_rank);
+    UTV_CUDA(cudaMemcpyAsync(c.h->h_rank, c.h->d_rank, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  }
+  UTV_CUDA(cudaMemcpyAsync(c.h->h_info, c.h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  UTV_CUDA(cudaMemcpyAsync(c.h->h_info + 2, c.h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  UTV_CUDA(cudaStreamSynchronize(st));
+  if (c.h->h_info[2]) fail(UTV_ERR_NUMERICAL, "NaN or Inf in A or B");
+  if (c.h->h_info[1]) fail(UTV_ERR_NUMERICAL, "Jacobi SVD of a diagonal block did not converge in 30 sweeps");
+  return want_rank ? *c.h->h_rank : -1;
+}
+
+// X = V(:, 0:r) T(0:r,0:r)^{-1} C(0:r, :) on device buffers.
+void solve_impl(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t ldt, const double* V, int64_t ldv,
+                const double* Cm, int64_t ldc, int64_t k, double* X, int64_t ldx) {
+  cudaStream_t st = c.st;
+  if (k <= 0) return;
+  if (r <= 0) { launch_set_zero(st, n, k, X, ldx); return; }
+  double* Zb = c.at(c.L.zsolve);
+  launch_copy(st, r, k, Cm, ldc, Zb, r);
+  constexpr int64_t SB = 256;
+  for (int64_t j0 = ((r - 1) / SB) * SB; j0 >= 0; j0 -= SB) {
+    const int64_t j1 = std::min(r, j0 + SB);
+    launch_trsv_block(st, j0, j1, T, ldt, Zb, r, k);
+    if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Zb + j0, r, 1.0, Zb, r);
+  }
+  c.gemm(false, false, n, k, r, 1.0, V, ldv, Zb, r, 0.0, X, ldx);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* utv_version(void) { return "utv-b200 0.1 sm_100a (FP64 DMMA)"; }
+
+utv_status utv_create(utv_handle* handle, int device, void* stream) {
+  if (!handle) return UTV_ERR_ARG;
+  *handle = nullptr;
+  utv_handle h = new (std::nothrow) utv_handle_s();
+  if (!h) return UTV_ERR_ALLOC;
+  h->device = device;
+  h->stream = (cudaStream_t)stream;
+  utv_status s = guarded(h, [&] {
+    int cnt = 0;
+    UTV_CUDA(cudaGetDeviceCount(&cnt));
+    if (device < 0 || device >= cnt) fail(UTV_ERR_ARG, "device ordinal out of range");
+    UTV_CUDA(cudaSetDevice(device));
+    UTV_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int coop = 0;
+    UTV_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    if (!coop) fail(UTV_ERR_UNSUPPORTED, "device does not support cooperative launch");
+    UTV_CUDA(cudaMalloc((void**)&h->bar, 64));
+    UTV_CUDA(cudaMemset(h->bar, 0, 64));
+    UTV_CUDA(cudaMalloc((void**)&h->info, 64 * sizeof(int)));
+    UTV_CUDA(cudaMalloc((void**)&h->flag, sizeof(int)));
+    UTV_CUDA(cudaMalloc((void**)&h->d_rank, sizeof(int64_t)));
+    UTV_CUDA(cudaMallocHost((void**)&h->h_rank, sizeof(int64_t)));
+    UTV_CUDA(cudaMallocHost((void**)&h->h_info, 4 * sizeof(int)));
+  });
+  if (s != UTV_OK) { utv_destroy(h); return s; }
+  *handle = h;
+  return UTV_OK;
+}
+
+utv_status utv_create_dist(utv_handle* handle, int, void*, const void*, int, int) {
+  if (handle) *handle = nullptr;
+  return UTV_ERR_UNSUPPORTED;
+}
+
+utv_status utv_destroy(utv_handle h) {
+  if (!h) return UTV_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream); else cudaDeviceSynchronize();
+  cudaFree(h->ws); cudaFree(h->bar); cudaFree(h->info); cudaFree(h->flag); cudaFree(h->d_rank);
+  cudaFree(h->vbuf); cudaFree(h->stage);
+  cudaFreeHost(h->h_rank); cudaFreeHost(h->h_info);
+  cudaGetLastError();
+  delete h;
+  return UTV_OK;
+}
+
+const char* utv_last_error(utv_handle h) { return h ? h->last_error.c_str() : "null handle"; }
+
+utv_status utv_set_stream(utv_handle h, void* stream) {
+  return guarded(h, [&] { h->stream = (cudaStream_t)stream; });
+}
+
+utv_status utv_synchronize(utv_handle h) {
+  return guarded(h, [&] { UTV_CUDA(cudaStreamSynchronize(h->stream)); });
+}
+
+utv_status utv_factor(utv_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* V, int64_t ldv, double* U,
+                      int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts* opts, int64_t* rank) {
+  return guarded(h, [&] {
+    check_opts(opts);
+    if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
+    if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
+    if (n > 0 && !A) fail(UTV_ERR_ARG, "A is NULL");
+    check_ld("lda", lda, m);
+    if (V) check_ld("ldv", ldv, n);
+    const bool want_u = U && (opts->flags & UTV_WANT_U);
+    if (want_u) check_ld("ldu", ldu, m);
+    if (B && k > 0) check_ld("ldb", ldb, m);
+    if (n == 0) { if (rank) *rank = 0; return; }
+    Ctx c = make_ctx(h, m, n, k, opts->block);
+    factor_impl(c, m, n, A, lda, V, ldv, want_u ? U : nullptr, ldu, (B && k > 0) ? B : nullptr, ldb, k, *opts);
+    int64_t r = finish_factor(c, n, A, lda, opts->tau, rank != nullptr);
+    if (rank) *rank = r;
+  });
+}
+
+utv_status utv_solve(utv_handle h, int64_t m, int64_t n, int64_t r, const double* T, int64_t ldt, const double* V,
+                     int64_t ldv, const double* C, int64_t ldc, int64_t k, double* X, int64_t ldx) {
+  return guarded(h, [&] {
+    if (m < 0 || n < 0 || k < 0 || r < 0 || r > n) fail(UTV_ERR_ARG, "bad dimension (need 0 <= r <= n)");
+    if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
+    check_ld("ldt", ldt, m); check_ld("ldv", ldv, n); check_ld("ldc", ldc, m); check_ld("ldx", ldx, n);
+    if (k == 0 || n == 0) return;
+    if (!X || (r > 0 && (!T || !V || !C))) fail(UTV_ERR_ARG, "NULL matrix");
+    Ctx c = make_ctx(h, m, n, k, 1);
+    solve_impl(c, n, r, T, ldt, V, ldv, C, ldc, k, X, ldx);
+  });
+}
+
+utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
+                     double* X, int64_t ldx, const utv_opts* opts, int64_t* rank) {
+  return guarded(h, [&] {
+    check_opts(opts);
+    if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
+    if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
+    check_ld("lda", lda, m);
+    if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
+    if ((n > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
+    if (n == 0) { if (rank) *rank = 0; return; }
+    cudaStream_t st = h->stream;
+    // host buffers (the end-to-end path): stage through device memory on the stream
+    const bool hA = !is_device_ptr(A), hB = k > 0 && !is_device_ptr(B), hX = k > 0 && !is_device_ptr(X);
+    size_t need = (hA ? (size_t)m * n : 0) + (hB ? (size_t)m * k : 0) + (hX ? (size_t)n * k : 0);
+    if (need) ensure_buf(&h->stage, &h->stage_doubles, need);
+    double* dA = A; int64_t dlda = lda;
+    double* dB = B; int64_t dldb = ldb;
+    double* dX = X; int64_t dldx = ldx;
+    size_t off = 0;
+    if (hA) { dA = h->stage + off; dlda = m; off += (size_t)m * n; copy2d(st, dA, m, A, lda, m, n, cudaMemcpyHostToDevice); }
+    if (hB) { dB = h->stage + off; dldb = m; off += (size_t)m * k; copy2d(st, dB, m, B, ldb, m, k, cudaMemcpyHostToDevice); }
+    if (hX) { dX = h->stage + off; dldx = n; off += (size_t)n * k; }
+    ensure_buf(&h->vbuf, &h->vbuf_doubles, (size_t)n * n);
+    Ctx c = make_ctx(h, m, n, k, opts->block);
+    factor_impl(c, m, n, dA, dlda, h->vbuf, n, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts);
+    int64_t r = finish_factor(c, n, dA, dlda, opts->tau, true);
+    if (k > 0) solve_impl(c, n, r, dA, dlda, h->vbuf, n, dB, dldb, k, dX, dldx);
+    if (hA) copy2d(st, A, lda, dA, m, m, n, cudaMemcpyDeviceToHost);
+    if (hB) copy2d(st, B, ldb, dB, m, m, k, cudaMemcpyDeviceToHost);
+    if (hX) copy2d(st, X, ldx, dX, n, n, k, cudaMemcpyDeviceToHost);
+    if (hA || hB || hX) UTV_CUDA(cudaStreamSynchronize(st));
+    if (rank) *rank = r;
+  });
+}
+
+// ---------------------------------------------------------------- step-level entry points
+utv_status utv_sketch(utv_handle h, uint64_t seed, int64_t step, int64_t row0, int64_t mrows, int64_t b, double* G,
+                      int64_t ldg) {
+  return guarded(h, [&] {
+    if (mrows < 0 || b < 0 || row0 < 0 || step < 0) fail(UTV_ERR_ARG, "negative argument");
+    if (mrows * b > 0 && !G) fail(UTV_ERR_ARG, "G is NULL");
+    check_ld("ldg", ldg, mrows);
+    launch_sketch(h->stream, seed, step, row0, mrows, b, G, ldg, h->num_sms);
+  });
+}
+
+utv_status utv_philox(utv_handle h, int64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  return guarded(h, [&] {
+    if (n < 0) fail(UTV_ERR_ARG, "n < 0");
+    if (n > 0 && (!ctr || !key || !out)) fail(UTV_ERR_ARG, "NULL pointer");
+    launch_philox_words(h->stream, ctr, key, n, out);
+  });
+}
+
+utv_status utv_hqr(utv_handle h, int64_t m, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
+                   double* T, int64_t ldt) {
+  return guarded(h, [&] {
+    if (w < 0 || m < w) fail(UTV_ERR_SHAPE, "need m >= w >= 0");
+    if (w == 0) return;
+    if (!P || !W || !tau || !T) fail(UTV_ERR_ARG, "NULL pointer");
+    check_ld("ldp", ldp, m); check_ld("ldw", ldw, m); check_ld("ldt", ldt, w);
+    Ctx c = make_ctx(h, m, w, 1, w);
+    panel_qr(h->stream, m, w, P, ldp, W, ldw, tau, T, ldt, c.pw);
+  });
+}
+
+utv_status utv_svd_small(utv_handle h, int64_t b, const double* R, int64_t ldr, double* Us, int64_t ldu,
+                         double* sigma, double* Vs, int64_t ldv, int32_t* sweeps) {
+  return guarded(h, [&] {
+    if (b < 1) fail(UTV_ERR_ARG, "b < 1");
+    if (b > 256) fail(UTV_ERR_UNSUPPORTED, "b > 256");
+    if (!R || !Us || !sigma || !Vs) fail(UTV_ERR_ARG, "NULL pointer");
+    check_ld("ldr", ldr, b); check_ld("ldu", ldu, b); check_ld("ldv", ldv, b);
+    Ctx c = make_ctx(h, b, b, 1, b);
+    UTV_CUDA(cudaMemsetAsync(h->info, 0, 4 * sizeof(int), h->stream));
+    svd_small(h->stream, b, R, ldr, Us, ldu, sigma, Vs, ldv, c.sw);
+    UTV_CUDA(cudaMemcpyAsync(h->h_info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    UTV_CUDA(cudaStreamSynchronize(h->stream));
+    if (sweeps) *sweeps = h->h_info[0];
+    if (h->h_info[1]) fail(UTV_ERR_NUMERICAL, "Jacobi did not converge in 30 sweeps");
+  });
+}
+
+utv_status utv_gemm(utv_handle h, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                    int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  return guarded(h, [&] {
+    if (M < 0 || N < 0 || K < 0) fail(UTV_ERR_ARG, "negative dimension");
+    if (M == 0 || N == 0) return;
+    check_ld("lda", lda, ta ? K : M); check_ld("ldb", ldb, tb ? N : K); check_ld("ldc", ldc, M);
+    if (!C || (K > 0 && (!A || !B))) fail(UTV_ERR_ARG, "NULL pointer");
+    size_t need = dgemm_workspace_doubles(M, N, K, h->num_sms);
+    if (need) ensure_buf(&h->ws, &h->ws_doubles, need);
+    dgemm(h->stream, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h->ws, h->ws_doubles,
+          h->num_sms);
+  });
+}
+
+utv_status utv_rank(utv_handle h, int64_t n, const double* T, int64_t ldt, double tau, int64_t* rank) {
+  return guarded(h, [&] {
+    if (n < 0 || !rank) fail(UTV_ERR_ARG, "bad argument");
+    if (!(tau >= 0.0 && tau < 1.0)) fail(UTV_ERR_ARG, "tau not in [0, 1)");
+    if (n == 0) { *rank = 0; return; }
+    check_ld("ldt", ldt, n);
+    launch_rank(h->stream, n, T, ldt, tau, h->d_rank);
+    UTV_CUDA(cudaMemcpyAsync(h->h_rank, h->d_rank, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    UTV_CUDA(cudaStreamSynchronize(h->stream));
+    *rank = *h->h_rank;
+  });
+}
+
+utv_status utv_profile(utv_handle h, int enable) {
+  return guarded(h, [&] {
+    if (enable) { h->prof.reset(); h->prof.on = true; }
+    else h->prof.on = false;
+  });
+}
+
+utv_status utv_profile_read(utv_handle h, utv_prof_entry* out) {
+  return guarded(h, [&] {
+    if (!out) fail(UTV_ERR_ARG, "out is NULL");
+    UTV_CUDA(cudaStreamSynchronize(h->stream));
+    for (int f = 0; f < kProfN; ++f) out[f] = utv_prof_entry{0, 0, 0.0, 0.0, 0.0};
+    for (const ProfRec& r : h->prof.recs) {
+      if (r.family < 0 || r.family >= kProfN) continue;
+      utv_prof_entry& e = out[r.family];
+      e.launches += r.launches;
+      e.calls += 1;
+      e.flops += r.flops;
+      e.bytes += r.bytes;
+      float ms = 0.f;
+      if (r.e0 && r.e1 && cudaEventElapsedTime(&ms, r.e0, r.e1) == cudaSuccess) e.ms += ms;
+      else cudaGetLastError();
+    }
+  });
+}
+
+}  // extern "C"
