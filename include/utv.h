@@ -108,7 +108,8 @@ utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const d
  * "Fast option" P:1114-1121; v34s): factor + Compute_rank + solve.  A and B are consumed
  * (overwritten by T and U^T B); X (n x k) written; *rank = r.  V is kept in the handle's
  * workspace.  A, B and X may be HOST pointers (pageable or pinned): they are then staged
- * through device buffers inside the call (the end-to-end path).
+ * through device buffers inside the call (the end-to-end path); host A and B are inputs only
+ * (left unchanged), a host X is written and the call returns after X has landed.
  */
 utv_status utv_lstsq(utv_handle handle, int64_t m, int64_t n, int64_t k, double* A, int64_t lda,
                      double* B, int64_t ldb, double* X, int64_t ldx, const utv_opts* opts,

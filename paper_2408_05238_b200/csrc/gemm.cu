@@ -16,17 +16,15 @@
 //    partials to a workspace, reduced in a fixed order by dgemm_splitk_reduce.
 #include "gemm.cuh"
 #include "prof.cuh"
+#include <cmath>
+#include <cstdlib>
 
 namespace utv {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
-constexpr int LD_MN = BM + 8;          // MN-major tile: [BK][BM + 8]
-constexpr int LD_K = BK + 4;           // K-major tile:  [BM][BK + 4]
-constexpr int TILE_DBL = (BK * LD_MN > BM * LD_K) ? BK * LD_MN : BM * LD_K;  // 2560
-constexpr int STAGE_DBL = 2 * TILE_DBL;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_DBL * sizeof(double);  // 160 KiB
+constexpr int BM = 128, BK = 16;
+constexpr int LD_K = BK + 4;           // K-major tile row: [BMN][BK + 4]
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -51,14 +49,38 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// Load one 128 x 16 operand tile (rows along MN, columns along K) into shared memory.
+// Shared-memory footprint (doubles) of one BMN x BK operand tile.
+template <int BMN, bool MN_MAJOR>
+constexpr int tile_doubles() { return MN_MAJOR ? BK * (BMN + 8) : BMN * LD_K; }
+
+// Tile configuration: warp tile 64 x 32 (4 x 4 m16n8 fragments), WARPS_N warps along N.
+//   WN = 4: 128 x 128 CTA tile, 256 threads, 1 CTA / SM (long-K products)
+//   WN = 2: 128 x  64 CTA tile, 128 threads, 2 CTAs / SM (short-K updates: one CTA's
+//           epilogue overlaps the other's main loop)
+template <bool TA, bool TB, int WN>
+struct Cfg {
+  static constexpr int BN = 32 * WN;
+  static constexpr int THREADS = 64 * WN;
+  static constexpr bool A_MN = !TA, B_MN = TB;
+  static constexpr int A_DBL = tile_doubles<BM, A_MN>();
+  static constexpr int B_DBL = tile_doubles<BN, B_MN>();
+  static constexpr int STAGE_DBL = A_DBL + B_DBL;
+  static constexpr int CTAS_PER_SM = WN == 4 ? 1 : 2;
+  static constexpr int SMEM_BUDGET = (WN == 4 ? 200 : 110) * 1024;
+  static constexpr int STAGES_FIT = SMEM_BUDGET / (STAGE_DBL * 8);
+  static constexpr int STAGES = STAGES_FIT > 4 ? 4 : STAGES_FIT;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_DBL * sizeof(double);
+  static_assert(STAGES >= 3, "not enough shared memory for a 3-stage pipeline");
+};
+
+// Load one BMN x 16 operand tile (rows along MN, columns along K) into shared memory.
 // MN_MAJOR: element (mn, k) at ptr[mn + k*ld]; otherwise at ptr[k + mn*ld].
-template <bool MN_MAJOR, int VEC>
+template <int BMN, bool MN_MAJOR, int VEC, int THREADS>
 __device__ __forceinline__ void load_tile(double* s, const double* __restrict__ g, int64_t ld, int64_t mn0,
                                           int64_t MN, int64_t k0, int64_t kend) {
   const int tid = threadIdx.x;
   if constexpr (MN_MAJOR) {
-    constexpr int CPR = BM / VEC;               // chunks per k-row
+    constexpr int CPR = BMN / VEC;              // chunks per k-row
     constexpr int NCH = BK * CPR;
 #pragma unroll
     for (int c = tid; c < NCH; c += THREADS) {
@@ -66,11 +88,11 @@ __device__ __forceinline__ void load_tile(double* s, const double* __restrict__ 
       const int64_t gk = k0 + kk, gm = mn0 + mm;
       int64_t rem = MN - gm; int valid = (gk < kend && rem > 0) ? (int)(rem < VEC ? rem : VEC) : 0;
       const double* src = valid ? g + gm + gk * ld : g;
-      cp_async<VEC>(smem_u32(s + kk * LD_MN + mm), src, valid * 8);
+      cp_async<VEC>(smem_u32(s + kk * (BMN + 8) + mm), src, valid * 8);
     }
   } else {
     constexpr int CPR = BK / VEC;
-    constexpr int NCH = BM * CPR;
+    constexpr int NCH = BMN * CPR;
 #pragma unroll
     for (int c = tid; c < NCH; c += THREADS) {
       const int mm = c / CPR, kk = (c % CPR) * VEC;
@@ -82,21 +104,22 @@ __device__ __forceinline__ void load_tile(double* s, const double* __restrict__ 
   }
 }
 
-template <bool MN_MAJOR>
+template <int BMN, bool MN_MAJOR>
 __device__ __forceinline__ double frag(const double* s, int mn, int k) {
-  return MN_MAJOR ? s[k * LD_MN + mn] : s[mn * LD_K + k];
+  return MN_MAJOR ? s[k * (BMN + 8) + mn] : s[mn * LD_K + k];
 }
 
 // A operand (m, k): TA=false -> A[m + k lda] (MN-major); TA=true -> A[k + m lda] (K-major).
 // B operand (k, n): TB=false -> B[k + n ldb] (K-major);  TB=true -> B[n + k ldb] (MN-major).
-template <bool TA, bool TB, int VEC>
-__global__ void __launch_bounds__(THREADS, 1)
+template <bool TA, bool TB, int VEC, int WN>
+__global__ void __launch_bounds__(Cfg<TA, TB, WN>::THREADS, Cfg<TA, TB, WN>::CTAS_PER_SM)
 dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
                   const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
                   int64_t k_chunk, double* __restrict__ partial) {
+  using CF = Cfg<TA, TB, WN>;
+  constexpr int BN = CF::BN, THREADS = CF::THREADS, STAGES = CF::STAGES;
+  constexpr bool A_MN = CF::A_MN, B_MN = CF::B_MN;
   extern __shared__ __align__(128) double smem[];
-  constexpr bool A_MN = !TA;
-  constexpr bool B_MN = TB;
 
   const int64_t n0 = (int64_t)blockIdx.x * BN;
   const int64_t m0 = (int64_t)blockIdx.y * BM;
@@ -105,7 +128,7 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
   const int nkt = (int)((kend - kbeg + BK - 1) / BK);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp >> 2, wn = warp & 3;       // 2 x 4 warps
+  const int wm = warp / WN, wn = warp % WN;      // 2 x WN warps
   const int g = lane >> 2, t = lane & 3;
 
   double acc[4][4][4];
@@ -116,49 +139,64 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
 
-  auto stage_a = [&](int s) { return smem + s * STAGE_DBL; };
-  auto stage_b = [&](int s) { return smem + s * STAGE_DBL + TILE_DBL; };
+  auto stage_a = [&](int s) { return smem + s * CF::STAGE_DBL; };
+  auto stage_b = [&](int s) { return smem + s * CF::STAGE_DBL + CF::A_DBL; };
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nkt) {
       const int64_t k0 = kbeg + (int64_t)s * BK;
-      load_tile<A_MN, VEC>(stage_a(s), A, lda, m0, M, k0, kend);
-      load_tile<B_MN, VEC>(stage_b(s), B, ldb, n0, N, k0, kend);
+      load_tile<BM, A_MN, VEC, THREADS>(stage_a(s), A, lda, m0, M, k0, kend);
+      load_tile<BN, B_MN, VEC, THREADS>(stage_b(s), B, ldb, n0, N, k0, kend);
     }
     cp_async_commit();
   }
 
-  for (int kt = 0; kt < nkt; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int pf = kt + STAGES - 1;
-      if (pf < nkt) {
-        const int s = pf % STAGES;
-        const int64_t k0 = kbeg + (int64_t)pf * BK;
-        load_tile<A_MN, VEC>(stage_a(s), A, lda, m0, M, k0, kend);
-        load_tile<B_MN, VEC>(stage_b(s), B, ldb, n0, N, k0, kend);
-      }
-      cp_async_commit();
+  // Software pipeline: the fragments of k-step s+1 are loaded (LDS) while the DMMAs of step s
+  // run (register double buffer), and the barrier that publishes the next stage is taken
+  // before the last k-step of the current one, so its latency overlaps 16 DMMAs.
+  double af[2][4][2], bf[2][4];
+  auto load_frags = [&](int buf, const double* sa, const double* sb, int kk) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int mr = wm * 64 + i * 16 + g;
+      af[buf][i][0] = frag<BM, A_MN>(sa, mr, kk + t);
+      af[buf][i][1] = frag<BM, A_MN>(sa, mr + 8, kk + t);
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[buf][j] = frag<BN, B_MN>(sb, wn * 32 + j * 8 + g, kk + t);
+  };
+
+  cp_async_wait<STAGES - 2>();
+  __syncthreads();
+  if (nkt > 0) load_frags(0, stage_a(0), stage_b(0), 0);
+
+  for (int kt = 0; kt < nkt; ++kt) {
     const double* sa = stage_a(kt % STAGES);
     const double* sb = stage_b(kt % STAGES);
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[4][2], bf[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int mr = wm * 64 + i * 16 + g;
-        af[i][0] = frag<A_MN>(sa, mr, kk + t);
-        af[i][1] = frag<A_MN>(sa, mr + 8, kk + t);
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int cur = ks & 1;
+      if (ks == BK / 4 - 1) {
+        // stage kt+1 must be visible to every warp; stage kt-1 has been fully read
+        cp_async_wait<STAGES - 3 >= 0 ? STAGES - 3 : 0>();
+        __syncthreads();
+        const int pf = kt + STAGES - 1;
+        if (pf < nkt) {
+          const int s = pf % STAGES;
+          const int64_t k0 = kbeg + (int64_t)pf * BK;
+          load_tile<BM, A_MN, VEC, THREADS>(stage_a(s), A, lda, m0, M, k0, kend);
+          load_tile<BN, B_MN, VEC, THREADS>(stage_b(s), B, ldb, n0, N, k0, kend);
+        }
+        cp_async_commit();
+        if (kt + 1 < nkt) load_frags(cur ^ 1, stage_a((kt + 1) % STAGES), stage_b((kt + 1) % STAGES), 0);
+      } else {
+        load_frags(cur ^ 1, sa, sb, (ks + 1) * 4);
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = frag<B_MN>(sb, wn * 32 + j * 8 + g, kk + t);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[i][j], af[i][0], af[i][1], bf[j]);
+        for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
     }
   }
   cp_async_wait<0>();
@@ -177,6 +215,27 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
           if (m < M && n < N) P[cm(m, n, M)] = acc[i][j][r];
         }
   } else {
+    if (beta != 0.0) {
+      // batch the C loads first (memory-level parallelism), then combine and store
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int64_t m = m0 + wm * 64 + i * 16 + g + (r >> 1) * 8;
+            const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
+            const double c = (m < M && n < N) ? __ldg(C + cm(m, n, ldc)) : 0.0;
+            acc[i][j][r] = alpha * acc[i][j][r] + beta * c;
+          }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[i][j][r] *= alpha;
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -185,11 +244,7 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
         for (int r = 0; r < 4; ++r) {
           const int64_t m = m0 + wm * 64 + i * 16 + g + (r >> 1) * 8;
           const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
-          if (m < M && n < N) {
-            double v = alpha * acc[i][j][r];
-            if (beta != 0.0) v += beta * C[cm(m, n, ldc)];
-            C[cm(m, n, ldc)] = v;
-          }
+          if (m < M && n < N) C[cm(m, n, ldc)] = acc[i][j][r];
         }
   }
 }
@@ -208,40 +263,75 @@ __global__ void dgemm_splitk_reduce(int64_t M, int64_t N, int S, double alpha, c
   }
 }
 
-template <bool TA, bool TB, int VEC>
+template <bool TA, bool TB, int VEC, int WN>
 void launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splits, int64_t kc,
               double* partial) {
+  using CF = Cfg<TA, TB, WN>;
   static bool attr_set = false;
-  auto kern = dgemm_dmma_kernel<TA, TB, VEC>;
+  auto kern = dgemm_dmma_kernel<TA, TB, VEC, WN>;
   if (!attr_set) {
-    UTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    UTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr_set = true;
   }
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
-  kern<<<grid, THREADS, SMEM_BYTES, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial);
+  dim3 grid((unsigned)((N + CF::BN - 1) / CF::BN), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
+  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial);
   UTV_CUDA(cudaGetLastError());
 }
 
-template <int VEC>
+template <int VEC, int WN>
 void dispatch(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splits,
               int64_t kc, double* partial) {
-  if (!ta && !tb) launch_t<false, false, VEC>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else if (ta && !tb) launch_t<true, false, VEC>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else if (!ta && tb) launch_t<false, true, VEC>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else launch_t<true, true, VEC>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  if (!ta && !tb) launch_t<false, false, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  else if (ta && !tb) launch_t<true, false, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  else if (!ta && tb) launch_t<false, true, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  else launch_t<true, true, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
 }
+
+int g_force_wn = 0;   // 0 = heuristic; 2 or 4 forces the tile width (benchmarking)
 
 }  // namespace
 
+void dgemm_force_tile_width(int wn) { g_force_wn = wn; }
+
+// Launch plan: tile width (WN) and split-K factor from a small cost model (waves of CTAs x
+// per-tile time + the split-K reduce traffic).  Fixes wave quantisation: e.g. 782 tiles on 148
+// SMs is 5.28 waves -> 6 (88%); split 3 gives 2346 tiles = 15.85 -> 16 waves (99%).
+struct Plan { int wn; int splits; int64_t kc; };
+
+static Plan make_plan(int64_t M, int64_t N, int64_t K, int num_sms, size_t work_doubles) {
+  static const int env_wn = [] {
+    const char* e = std::getenv("UTV_GEMM_WN");        // benchmarking override: 2 or 4
+    return e ? std::atoi(e) : 0;
+  }();
+  if (!g_force_wn && (env_wn == 2 || env_wn == 4)) g_force_wn = env_wn;
+  Plan best{K <= 1024 ? 2 : 4, 1, K};
+  if (g_force_wn) best.wn = g_force_wn;
+  double best_t = 1e300;
+  for (int wn : {2, 4}) {
+    if (g_force_wn && wn != g_force_wn) continue;
+    if (!g_force_wn && K > 1024 && wn == 2) continue;      // long K: wide tiles (operand reuse)
+    if (!g_force_wn && K <= 1024 && wn == 4) continue;     // short K: 2 CTAs / SM overlap epilogues
+    const int bn = 32 * wn, ctas = wn == 4 ? 1 : 2;
+    const double slots = (double)num_sms * ctas;
+    const double tiles = (double)((M + BM - 1) / BM) * (double)((N + bn - 1) / bn);
+    const double rate = 37.2e12 * 0.85 / slots;            // flop/s per CTA slot
+    for (int s = 1; s <= 128; ++s) {
+      if (s > 1 && (K / s < 256 || (size_t)s * (size_t)M * (size_t)N > work_doubles)) break;
+      const int64_t kc = s == 1 ? K : ((K + s - 1) / s + BK - 1) / BK * BK;
+      const int sp = (int)((K + kc - 1) / kc);
+      const double waves = std::ceil(tiles * sp / slots);
+      double t = waves * (2.0 * BM * bn * (double)kc / rate + 2.5e-6);
+      if (sp > 1) t += 8.0 * (double)M * (double)N * (sp + 1) / 5.0e12 + 4e-6;
+      if (t < best_t * 0.995) { best_t = t; best = Plan{wn, sp, kc}; }
+    }
+  }
+  return best;
+}
+
 int dgemm_split_count(int64_t M, int64_t N, int64_t K, int num_sms) {
-  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  if (tiles >= num_sms || K < 4 * 256) return 1;
-  int64_t s = (2 * (int64_t)num_sms + tiles - 1) / tiles;
-  s = std::min<int64_t>(s, K / 256);                 // >= 256 deep per split
-  s = std::min<int64_t>(s, 128);
-  return (int)std::max<int64_t>(s, 1);
+  return make_plan(M, N, K, num_sms, (size_t)-1).splits;
 }
 
 size_t dgemm_workspace_doubles(int64_t M, int64_t N, int64_t K, int num_sms) {
@@ -263,22 +353,20 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
   }
   const bool aligned = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 == 0) &&
                        (lda % 2 == 0) && (ldb % 2 == 0);
-  int splits = dgemm_split_count(M, N, K, num_sms);
-  if (splits > 1 && (size_t)splits * (size_t)M * (size_t)N > work_doubles) {
-    splits = (int)std::max<size_t>(1, work_doubles / ((size_t)M * (size_t)N));
-  }
-  int64_t kc = K;
-  if (splits > 1) {
-    kc = ((K + splits - 1) / splits + BK - 1) / BK * BK;
-    splits = (int)((K + kc - 1) / kc);
-  }
+  const Plan plan = make_plan(M, N, K, num_sms, work ? work_doubles : 0);
+  const int splits = plan.splits;
+  const int64_t kc = plan.kc;
   double* partial = splits > 1 ? work : nullptr;
   ProfScope prof(st, kProfGemm, splits > 1 ? 2 : 1, 2.0 * (double)M * (double)N * (double)K,
                  8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2.0 : 1.0)));
-  if (aligned)
-    dispatch<2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else
-    dispatch<1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  const int wn = plan.wn;
+  if (aligned) {
+    if (wn == 2) dispatch<2, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+    else dispatch<2, 4>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  } else {
+    if (wn == 2) dispatch<1, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+    else dispatch<1, 4>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  }
   if (splits > 1) {
     const int64_t total = M * N;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * (int64_t)num_sms);

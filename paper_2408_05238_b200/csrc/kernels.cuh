@@ -12,7 +12,7 @@ void launch_philox_words(cudaStream_t st, const uint32_t* ctr, const uint32_t* k
 
 // ---- a3/a5: Householder panel QR (panel_qr.cu) -------------------------------------------
 struct PanelWork {
-  double* part;          // >= num_sms * 32 doubles (per-CTA partial sums)
+  double* part;          // >= 2 * num_sms * 64 doubles (double-buffered per-CTA partials)
   double* z1;            // >= 32 * w doubles
   double* z2;            // >= 32 * w doubles
   double* gram;          // >= w * w doubles

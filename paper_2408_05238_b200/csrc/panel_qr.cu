@@ -53,6 +53,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
            unsigned* __restrict__ bar) {
   __shared__ double red_w[(QR_THREADS / 32) * NBMAX];
   __shared__ double red[NBMAX];
+  __shared__ double piv[NBMAX];      // pivot row j (published by its owner)
   __shared__ double sw[NBMAX];       // w_l = v^T P[:, l]
   __shared__ double ssg[NBMAX];      // s_p = W[:, p]^T v
   __shared__ double sT[NBMAX * NBMAX];
@@ -91,8 +92,17 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       if (l < nb) acc[l] += x * P[cm(i, l, ldp)];
   }
 
+  // part is double-buffered by column parity: slot (buf, c) holds CTA c's partial sums
+  // [0, nb) and, for the CTA owning the pivot row j, that row's values P[j, l] at [NBMAX + l].
+  // A CTA can run at most one column ahead of the slowest (it blocks in the next barrier), so
+  // the writes for column j+1 never touch the buffer still being read for column j, and the
+  // owner may update row j in place while the others use the published copy.
+  auto slot = [&](int buf, unsigned c) { return part + ((size_t)buf * G + c) * (2 * NBMAX); };
   for (int j = 0; j < nb; ++j) {
-    block_reduce_store(acc, nb, red_w, part + (size_t)blockIdx.x * NBMAX);
+    const int buf = j & 1;
+    const unsigned owner = (unsigned)(j / L);
+    block_reduce_store(acc, nb, red_w, slot(buf, blockIdx.x));
+    if (blockIdx.x == owner && tid >= j && tid < nb) __stcg(slot(buf, owner) + NBMAX + tid, P[cm(j, tid, ldp)]);
     grid_sync(bar, G, gen);
     {
       // fixed-order reduction of the G partials (identical in every CTA): warp w owns the
@@ -100,14 +110,15 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       const int warp = tid >> 5, lane = tid & 31;
       for (int v = warp; v < nb; v += QR_THREADS / 32) {
         double s = 0.0;
-        for (unsigned c = lane; c < G; c += 32) s += __ldcg(part + (size_t)c * NBMAX + v);
+        for (unsigned c = lane; c < G; c += 32) s += __ldcg(slot(buf, c) + v);
         s = warp_sum(s);
         if (lane == 0) red[v] = s;
       }
+      if (tid >= j && tid < nb) piv[tid] = __ldcg(slot(buf, owner) + NBMAX + tid);
     }
     __syncthreads();
     if (tid == 0) {
-      const double alpha = __ldcg(P + cm(j, j, ldp));
+      const double alpha = piv[j];
       const double xi = sqrt(red[j]);
       double t, beta, scal;
       if (xi == 0.0) {
@@ -122,7 +133,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     __syncthreads();
     const double tj = s_tau, scal = s_scal;
     if (tid < nb) {
-      if (tid > j) sw[tid] = __ldcg(P + cm(j, tid, ldp)) + red[tid] * scal;
+      if (tid > j) sw[tid] = piv[tid] + red[tid] * scal;
       else if (tid < j) ssg[tid] = __ldcg(W + cm(j, tid, ldw)) + red[tid] * scal;
     }
     __syncthreads();

@@ -123,7 +123,7 @@ Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
   L.sX = take((size_t)b * b);
   L.sQ = take((size_t)b * b);
   L.stau = take(b);
-  L.part = take((size_t)num_sms * 32);
+  L.part = take((size_t)num_sms * 128);   // 2 buffers x G x (32 sums + 32 pivot values)
   L.pz1 = take((size_t)32 * b);
   L.pz2 = take((size_t)32 * b);
   L.gram = take((size_t)b * b);
@@ -437,10 +437,9 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     factor_impl(c, m, n, dA, dlda, h->vbuf, n, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts);
     int64_t r = finish_factor(c, n, dA, dlda, opts->tau, true);
     if (k > 0) solve_impl(c, n, r, dA, dlda, h->vbuf, n, dB, dldb, k, dX, dldx);
-    if (hA) copy2d(st, A, lda, dA, m, m, n, cudaMemcpyDeviceToHost);
-    if (hB) copy2d(st, B, ldb, dB, m, m, k, cudaMemcpyDeviceToHost);
+    // host A / B are inputs only: they are not written back (see utv.h)
     if (hX) copy2d(st, X, ldx, dX, n, n, k, cudaMemcpyDeviceToHost);
-    if (hA || hB || hX) UTV_CUDA(cudaStreamSynchronize(st));
+    if (hX) UTV_CUDA(cudaStreamSynchronize(st));
     if (rank) *rank = r;
   });
 }

@@ -260,11 +260,13 @@ def test_deterministic_reruns(utv):
 def test_host_buffers_end_to_end(utv):
     M = gen.GpMatrix(400, 300, 140, seed=15)
     B, X0 = M.known_rhs(k=2)
-    A_h = torch.from_numpy(np.ascontiguousarray(M.A.T)).t()            # column-major host tensor
-    B_h = torch.from_numpy(np.ascontiguousarray(B.T)).t()
+    A_h = torch.from_numpy(M.A.T.copy()).t()            # column-major host tensors (own copies)
+    B_h = torch.from_numpy(B.T.copy()).t()
+    A_keep, B_keep = A_h.clone(), B_h.clone()
     X_h = torch.zeros((2, 300), dtype=torch.float64).t()
     h = utv.default_handle()
     r = h.lstsq(A_h, B_h, X_h, utv.Opts(block=64, power_iters=1, seed=1))
+    assert torch.equal(A_h, A_keep) and torch.equal(B_h, B_keep)      # host inputs left unchanged
     Xo, ro = oracle.lstsq(M.A, B, b=64, q=1, seed=1)
     assert r == ro == 140
     assert np.linalg.norm(X_h.numpy() - Xo) <= 1e-9 * np.linalg.norm(Xo)
