@@ -56,10 +56,15 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
       if (tid < 2 * JBLK) s_gcol[tid] = tid < JBLK ? bp * JBLK + tid : bq * JBLK + (tid - JBLK);
       if (tid == 0) s_rot = 0;
       __syncthreads();
-      for (int e = tid; e < 2 * JBLK * bw; e += JT) {
-        const int col = e / bw, row = e % bw, gc = s_gcol[col];
-        sW[e] = gc < bw ? __ldcg(W + (size_t)gc * bw + row) : 0.0;
-        sJ[e] = gc < bw ? __ldcg(J + (size_t)gc * bw + row) : 0.0;
+      // stage the 32 columns (all loads of a thread in flight together: <= 16 per matrix)
+#pragma unroll
+      for (int it = 0; it < 2 * JBLK * 256 / JT; ++it) {
+        const int e = tid + it * JT;
+        if (e < 2 * JBLK * bw) {
+          const int col = e / bw, row = e % bw, gc = s_gcol[col];
+          sW[e] = gc < bw ? __ldcg(W + (size_t)gc * bw + row) : 0.0;
+          sJ[e] = gc < bw ? __ldcg(J + (size_t)gc * bw + row) : 0.0;
+        }
       }
       __syncthreads();
       for (int ir = 0; ir < 2 * JBLK - 1; ++ir) {
@@ -100,11 +105,15 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
         }
         __syncthreads();
       }
-      for (int e = tid; e < 2 * JBLK * bw; e += JT) {
-        const int col = e / bw, row = e % bw, gc = s_gcol[col];
-        if (gc < bw) {
-          __stcg(W + (size_t)gc * bw + row, sW[e]);
-          __stcg(J + (size_t)gc * bw + row, sJ[e]);
+#pragma unroll
+      for (int it = 0; it < 2 * JBLK * 256 / JT; ++it) {
+        const int e = tid + it * JT;
+        if (e < 2 * JBLK * bw) {
+          const int col = e / bw, row = e % bw, gc = s_gcol[col];
+          if (gc < bw) {
+            __stcg(W + (size_t)gc * bw + row, sW[e]);
+            __stcg(J + (size_t)gc * bw + row, sJ[e]);
+          }
         }
       }
       if (tid == 0 && s_rot) atomicAdd(rot + sweep, s_rot);

@@ -21,6 +21,8 @@ namespace utv {
 namespace {
 constexpr int NBMAX = 32;
 constexpr int QR_THREADS = 256;
+constexpr int SROW = NBMAX + 1;            // padded shared-memory row (conflict-free per column)
+constexpr int SMEM_ROWS_MAX = 768;         // CTA rows cached in shared memory (<= 198 KiB)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -28,34 +30,57 @@ __device__ __forceinline__ double warp_sum(double v) {
   return __shfl_sync(0xffffffffu, v, 0);
 }
 
-// acc[v], v < nb: p < j -> sum x_i W[i,p]; v == j -> sum x_i^2; v > j -> sum x_i P[i,v]
-// (rows i > j of the CTA range).  Block-reduce and store this CTA's partials.
-__device__ __forceinline__ void block_reduce_store(double (&acc)[NBMAX], int nb, double* red_w, double* part_out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Transpose-reduce 32 per-lane values over the warp with 31 shuffles (instead of 32 x 5): after
+// the 5 halving levels lane l holds the warp total of value index l.  Fixed order (deterministic).
+__device__ __forceinline__ double warp_transpose_reduce(double (&a)[NBMAX]) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int v = 0; v < NBMAX; ++v) {
-    if (v < nb) {
-      double s = warp_sum(acc[v]);
-      if (lane == 0) red_w[warp * NBMAX + v] = s;
+  for (int lvl = 0; lvl < 5; ++lvl) {
+    const int o = 16 >> lvl;               // exchange partner distance == half the live width
+    const bool upper = lane & o;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < o) {
+        const double send = upper ? a[i] : a[i + o];
+        const double keep = upper ? a[i + o] : a[i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
     }
   }
+  return a[0];
+}
+
+// Block-reduce acc[0..nb) (rows i > j of this CTA) and store this CTA's partials.
+template <bool GLOBAL>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NBMAX], int nb, double* red_w, double* part_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double s = warp_transpose_reduce(acc);
+  red_w[warp * NBMAX + lane] = s;
   __syncthreads();
   if (threadIdx.x < nb) {
-    double s = 0.0;
-    for (int w = 0; w < QR_THREADS / 32; ++w) s += red_w[w * NBMAX + threadIdx.x];
-    __stcg(part_out + threadIdx.x, s);
+    double t = 0.0;
+    for (int w = 0; w < QR_THREADS / 32; ++w) t += red_w[w * NBMAX + threadIdx.x];
+    if constexpr (GLOBAL) __stcg(part_out + threadIdx.x, t);
+    else part_out[threadIdx.x] = t;
   }
 }
 
+// Unblocked Householder QR of the R x nb sub-panel P (rows 0..R-1 from its diagonal),
+// LAPACK storage during the kernel (R on/above the diagonal, v strictly below), explicit W and
+// zeros below R written at the end.  CTA c owns rows [c L, (c+1) L); SMEM: those rows live in
+// shared memory for the whole kernel, else each row is re-read from global (L2) per column with
+// all its loads in flight.  One grid barrier per column.
+template <bool SMEM>
 __global__ void __launch_bounds__(QR_THREADS, 1)
 qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __restrict__ W, int64_t ldw, int64_t wtop,
            double* __restrict__ tau, double* __restrict__ T, int64_t ldt, double* __restrict__ part,
            unsigned* __restrict__ bar) {
+  extern __shared__ double sp[];             // [L][SROW] (SMEM only)
   __shared__ double red_w[(QR_THREADS / 32) * NBMAX];
   __shared__ double red[NBMAX];
-  __shared__ double piv[NBMAX];      // pivot row j (published by its owner)
-  __shared__ double sw[NBMAX];       // w_l = v^T P[:, l]
-  __shared__ double ssg[NBMAX];      // s_p = W[:, p]^T v
+  __shared__ double piv[NBMAX];              // row j: W values (< j) and P values (>= j)
+  __shared__ double sw[NBMAX];               // w_l = v^T P[:, l]
+  __shared__ double ssg[NBMAX];              // s_p = W[:, p]^T v
   __shared__ double sT[NBMAX * NBMAX];
   __shared__ double s_tau, s_beta, s_scal;
   __shared__ unsigned s_gen;
@@ -65,59 +90,76 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   const int64_t L = (R + G - 1) / G;
   const int64_t r0 = (int64_t)blockIdx.x * L;
   const int64_t r1 = min(R, r0 + L);
-  unsigned gen = 0;
-  if (tid == 0) { s_gen = *((volatile unsigned*)bar + 1); }
-  __syncthreads();
-  gen = s_gen;
-
-  // zero the rows above the sub-panel in W (columns 0..nb-1)
+  if (tid == 0) s_gen = *((volatile unsigned*)bar + 1);
   if (blockIdx.x == 0) {
-    for (int64_t e = tid; e < wtop * nb; e += QR_THREADS) {
+    for (int64_t e = tid; e < wtop * nb; e += QR_THREADS) {   // rows above the sub-panel in W
       const int64_t i = e % wtop, c = e / wtop;
       W[c * ldw + (i - wtop)] = 0.0;
     }
     for (int e = tid; e < NBMAX * NBMAX; e += QR_THREADS) sT[e] = 0.0;
   }
+  if constexpr (SMEM) {
+    for (int64_t e = tid; e < (r1 - r0) * nb; e += QR_THREADS) {
+      const int64_t il = e % (r1 - r0), c = e / (r1 - r0);
+      sp[il * SROW + c] = P[cm(r0 + il, c, ldp)];
+    }
+  }
+  __syncthreads();
+  unsigned gen = s_gen;
 
   double acc[NBMAX];
 #pragma unroll
   for (int v = 0; v < NBMAX; ++v) acc[v] = 0.0;
-  // reduction for column 0
-  for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
+  for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {        // column 0: rows i > 0
     if (i < 1) continue;
-    const double x = P[cm(i, 0, ldp)];
-    acc[0] += x * x;
+    const double x0 = SMEM ? sp[(i - r0) * SROW] : P[cm(i, 0, ldp)];
 #pragma unroll
-    for (int l = 1; l < NBMAX; ++l)
-      if (l < nb) acc[l] += x * P[cm(i, l, ldp)];
+    for (int p = 0; p < NBMAX; ++p)
+      if (p < nb) acc[p] += x0 * (SMEM ? sp[(i - r0) * SROW + p] : P[cm(i, p, ldp)]);
   }
 
-  // part is double-buffered by column parity: slot (buf, c) holds CTA c's partial sums
-  // [0, nb) and, for the CTA owning the pivot row j, that row's values P[j, l] at [NBMAX + l].
-  // A CTA can run at most one column ahead of the slowest (it blocks in the next barrier), so
-  // the writes for column j+1 never touch the buffer still being read for column j, and the
-  // owner may update row j in place while the others use the published copy.
+  // part: double-buffered by column parity; slot (buf, c) = CTA c's partial sums at [0, nb) and,
+  // for the CTA owning pivot row j, that row at [NBMAX, NBMAX + nb).  A CTA runs at most one column
+  // ahead of the slowest, so writes for column j+1 never touch the buffer read for column j, and
+  // the owner updates row j in place while the others use the published copy.
   auto slot = [&](int buf, unsigned c) { return part + ((size_t)buf * G + c) * (2 * NBMAX); };
   for (int j = 0; j < nb; ++j) {
     const int buf = j & 1;
     const unsigned owner = (unsigned)(j / L);
-    block_reduce_store(acc, nb, red_w, slot(buf, blockIdx.x));
-    if (blockIdx.x == owner && tid >= j && tid < nb) __stcg(slot(buf, owner) + NBMAX + tid, P[cm(j, tid, ldp)]);
-    grid_sync(bar, G, gen);
-    {
-      // fixed-order reduction of the G partials (identical in every CTA): warp w owns the
-      // values v = w, w+8, ...; lane l sums CTAs c = l, l+32, ...; then a fixed butterfly.
+    if (G == 1) {
+      block_reduce_store<false>(acc, nb, red_w, red);
+      if (tid < nb) piv[tid] = SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)];
+      __syncthreads();
+    } else {
+      block_reduce_store<true>(acc, nb, red_w, slot(buf, blockIdx.x));
+      if (blockIdx.x == owner && tid < nb)
+        __stcg(slot(buf, owner) + NBMAX + tid, SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)]);
+      grid_sync(bar, G, gen);
+      // fixed-order reduction of the G partials (identical in every CTA): warp w owns values
+      // v = w + 8u; lane l sums CTAs c = l + 32q with all loads in flight, then a fixed butterfly
       const int warp = tid >> 5, lane = tid & 31;
-      for (int v = warp; v < nb; v += QR_THREADS / 32) {
-        double s = 0.0;
-        for (unsigned c = lane; c < G; c += 32) s += __ldcg(slot(buf, c) + v);
+      constexpr int QMAX = 5;                // G <= 160
+      double vals[NBMAX / 8][QMAX];
+#pragma unroll
+      for (int u = 0; u < NBMAX / 8; ++u)
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          const unsigned c = lane + 32u * q;
+          const int v = warp + 8 * u;
+          vals[u][q] = (c < G && v < nb) ? __ldcg(slot(buf, c) + v) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < NBMAX / 8; ++u) {
+        double s = vals[u][0];
+#pragma unroll
+        for (int q = 1; q < QMAX; ++q) s += vals[u][q];
         s = warp_sum(s);
-        if (lane == 0) red[v] = s;
+        if (lane == 0 && warp + 8 * u < nb) red[warp + 8 * u] = s;
       }
-      if (tid >= j && tid < nb) piv[tid] = __ldcg(slot(buf, owner) + NBMAX + tid);
+      if (tid < nb) piv[tid] = __ldcg(slot(buf, owner) + NBMAX + tid);
+      __syncthreads();
     }
-    __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {                          // dlarfg on x = P[j:, j]
       const double alpha = piv[j];
       const double xi = sqrt(red[j]);
       double t, beta, scal;
@@ -131,10 +173,10 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       s_tau = t; s_beta = beta; s_scal = scal;
     }
     __syncthreads();
-    const double tj = s_tau, scal = s_scal;
+    const double tj = s_tau, scal = s_scal, beta = s_beta;
     if (tid < nb) {
-      if (tid > j) sw[tid] = piv[tid] + red[tid] * scal;
-      else if (tid < j) ssg[tid] = __ldcg(W + cm(j, tid, ldw)) + red[tid] * scal;
+      if (tid > j) sw[tid] = piv[tid] + red[tid] * scal;       // v^T P[:, l], v_j = 1
+      else if (tid < j) ssg[tid] = piv[tid] + red[tid] * scal; // W[:, p]^T v
     }
     __syncthreads();
     if (blockIdx.x == 0) {
@@ -150,32 +192,44 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     for (int v = 0; v < NBMAX; ++v) acc[v] = 0.0;
     const bool next = (j + 1 < nb);
     for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
-      if (i < j) { W[cm(i, j, ldw)] = 0.0; continue; }
-      double v;
-      if (i == j) { v = 1.0; P[cm(j, j, ldp)] = s_beta; }
-      else { v = P[cm(i, j, ldp)] * scal; P[cm(i, j, ldp)] = 0.0; }
-      W[cm(i, j, ldw)] = v;
-      const double tv = tj * v;
-      const bool acc_next = next && (i > j + 1);
-      double xn = 0.0;
+      if (i < j) continue;                   // rows above the pivot: untouched
+      // stream the row once (registers: acc only); j is runtime, so every index is static and
+      // selected with unrolled compares
+      auto ld = [&](int c) { return SMEM ? sp[(i - r0) * SROW + c] : P[cm(i, c, ldp)]; };
+      auto st = [&](int c, double x) {
+        if (SMEM) sp[(i - r0) * SROW + c] = x; else P[cm(i, c, ldp)] = x;
+      };
+      double xj = 0.0, xj1 = 0.0, swj1 = 0.0;
 #pragma unroll
-      for (int l = 1; l < NBMAX; ++l) {
-        if (l > j && l < nb) {
-          double pl = P[cm(i, l, ldp)];
-          if (tj != 0.0) { pl -= tv * sw[l]; P[cm(i, l, ldp)] = pl; }
-          if (l == j + 1) xn = pl;
-          else if (acc_next) acc[l] += xn * pl;
-        }
+      for (int c = 0; c < NBMAX; ++c) {
+        if (c == j) xj = ld(c);
+        if (c == j + 1 && c < nb) { xj1 = ld(c); swj1 = sw[c]; }
       }
-      if (acc_next) {
+      const double v = (i == j) ? 1.0 : xj * scal;
+      const double newj = (i == j) ? beta : v;   // v stored below the diagonal (LAPACK)
+      const double tv = tj * v;
+      const bool acc_next = next && i > j + 1; // column j+1: norm, v^T-products, Gram column
+      const double xn = xj1 - tv * swj1;
 #pragma unroll
-        for (int p = 0; p < NBMAX; ++p) {
-          if (p <= j) acc[p] += xn * (p == j ? v : W[cm(i, p, ldw)]);
-          else if (p == j + 1) acc[p] += xn * xn;
+      for (int c = 0; c < NBMAX; ++c) {
+        if (c < nb) {
+          double val;
+          if (c == j) val = newj;
+          else if (c > j) val = ld(c) - tv * sw[c];
+          else val = acc_next ? ld(c) : 0.0;
+          if (c >= j) st(c, val);
+          if (acc_next) acc[c] += xn * val;
         }
       }
     }
     __syncthreads();
+  }
+  // write back: P = R (upper) / 0 (below); W = explicit unit-lower Householder vectors
+  for (int64_t e = tid; e < (r1 - r0) * nb; e += QR_THREADS) {
+    const int64_t il = e % (r1 - r0), c = e / (r1 - r0), i = r0 + il;
+    const double x = SMEM ? sp[il * SROW + c] : P[cm(i, c, ldp)];
+    P[cm(i, c, ldp)] = i <= c ? x : 0.0;
+    W[cm(i, c, ldw)] = i < c ? 0.0 : (i == c ? 1.0 : x);
   }
   if (blockIdx.x == 0) {
     for (int e = tid; e < nb * nb; e += QR_THREADS) {
@@ -194,14 +248,26 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
   for (int64_t jb = 0; jb < w; jb += NBMAX) {
     const int nb = (int)std::min<int64_t>(NBMAX, w - jb);
     const int64_t R = rows - jb;
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(pw.num_sms, (R + 127) / 128));
+    // one CTA (no grid barrier) up to 1024 rows; else ~256+ rows per CTA, at most one per SM
+    const int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(std::min(pw.num_sms, 160),
+                                                                            (R + 255) / 256));
+    const int64_t Lr = (R + G - 1) / G;
+    const bool smem = Lr <= SMEM_ROWS_MAX;
     int64_t Rv = R; int nbv = nb; double* Pb = P + cm(jb, jb, ldp); double* Wb = W + cm(jb, jb, ldw);
     int64_t wtop = jb; double* taub = tau + jb; double* Tb = T + cm(jb, jb, ldt);
     void* args[] = {&Rv, &nbv, &Pb, (void*)&ldp, &Wb, (void*)&ldw, &wtop, &taub, &Tb, (void*)&ldt,
                     (void*)&pw.part, (void*)&pw.bar};
     {
       ProfScope prof(st, kProfPanel, 1, 2.0 * (double)R * nb * nb, 16.0 * (double)R * nb);
-      UTV_CUDA(cudaLaunchCooperativeKernel((void*)qr2_kernel, dim3(G), dim3(QR_THREADS), args, 0, st));
+      static bool attr = false;
+      if (!attr) {
+        UTV_CUDA(cudaFuncSetAttribute(qr2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(SMEM_ROWS_MAX * SROW * sizeof(double))));
+        attr = true;
+      }
+      const size_t smem_bytes = smem ? (size_t)Lr * SROW * sizeof(double) : 0;
+      UTV_CUDA(cudaLaunchCooperativeKernel(smem ? (void*)qr2_kernel<true> : (void*)qr2_kernel<false>, dim3(G),
+                                           dim3(QR_THREADS), args, smem_bytes, st));
     }
     const int64_t wr = w - jb - nb;
     if (wr > 0) {

@@ -22,7 +22,10 @@ struct utv_handle_s {
   // workspace arena (device)
   double* ws = nullptr;
   size_t ws_doubles = 0;
-  unsigned* bar = nullptr;       // grid-barrier state: [0] count, [1] generation
+  unsigned* bar = nullptr;       // grid-barrier state: [0] count, [1] generation (main stream)
+  unsigned* bar2 = nullptr;      // grid-barrier state of the SVD side stream
+  cudaStream_t side = nullptr;   // a7 (small SVD + its 4 updates) overlaps the next step's sketch
+  cudaEvent_t ev_panel = nullptr, ev_svd = nullptr;
   int* info = nullptr;           // Jacobi sweeps / failure flag
   int* flag = nullptr;           // finiteness flag
   int64_t* d_rank = nullptr;
@@ -87,7 +90,8 @@ void ensure_buf(double** p, size_t* have, size_t need) {
 struct Layout {
   size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, Tu, tauu, Z1, Z2, tmp, R, Us, Vs, sig;
   size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve;
-  size_t gemm_doubles;
+  size_t part2, pz1b, pz2b, gram2, px2, gemm2, tmp2;
+  size_t gemm_doubles, gemm2_doubles;
   size_t total;
 };
 
@@ -129,8 +133,19 @@ Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
   L.gram = take((size_t)b * b);
   L.px = take((size_t)b * 32);
   L.zsolve = take((size_t)n * std::max<int64_t>(k, 1));
-  L.gemm_doubles = std::max<size_t>((size_t)128 * b * std::max<int64_t>(b, 32), (size_t)1 << 22);
+  // split-K partials: the b x b Gram products (<= 128 b^2) and up to 4 splits of the long-K
+  // max(m,n) x b sketch products (wave-quantisation fix, see gemm.cu make_plan)
+  L.gemm_doubles = std::max<size_t>({(size_t)128 * b * std::max<int64_t>(b, 32), (size_t)1 << 22, 4 * mx * b});
   L.gemm = take(L.gemm_doubles);
+  // side-stream (SVD) copies of the panel workspace
+  L.part2 = take((size_t)num_sms * 128);
+  L.pz1b = take((size_t)32 * b);
+  L.pz2b = take((size_t)32 * b);
+  L.gram2 = take((size_t)b * b);
+  L.px2 = take((size_t)b * 32);
+  L.gemm2_doubles = std::max<size_t>((size_t)128 * b * std::max<int64_t>(b, 32), (size_t)1 << 20);
+  L.gemm2 = take(L.gemm2_doubles);
+  L.tmp2 = take(std::max<size_t>(mx * b, (size_t)b * nk));
   L.total = off;
   return L;
 }
@@ -140,12 +155,17 @@ struct Ctx {
   cudaStream_t st;
   Layout L;
   double* w;
-  PanelWork pw;
-  SvdWork sw;
+  cudaStream_t side;
+  PanelWork pw, pw2;
+  SvdWork sw;                    // uses pw2: runs on the side stream
   double* at(size_t off) const { return w + off; }
   void gemm(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
             const double* B, int64_t ldb, double beta, double* C, int64_t ldc) const {
     dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, at(L.gemm), L.gemm_doubles, h->num_sms);
+  }
+  void gemm_side(bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                 const double* B, int64_t ldb, double beta, double* C, int64_t ldc) const {
+    dgemm(side, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, at(L.gemm2), L.gemm2_doubles, h->num_sms);
   }
 };
 
@@ -157,10 +177,14 @@ Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
   ensure_buf(&h->ws, &h->ws_doubles, c.L.total);
   c.w = h->ws;
   const Layout& L = c.L;
+  c.side = h->side;
+  // the main-stream panel kernels leave 16 SMs free for the concurrent side-stream Jacobi
   c.pw = PanelWork{c.at(L.part), c.at(L.pz1), c.at(L.pz2), c.at(L.gram), c.at(L.px), c.at(L.gemm), L.gemm_doubles,
-                   h->bar, h->num_sms};
+                   h->bar, std::max(1, h->num_sms - 16)};
+  c.pw2 = PanelWork{c.at(L.part2), c.at(L.pz1b), c.at(L.pz2b), c.at(L.gram2), c.at(L.px2), c.at(L.gemm2),
+                    L.gemm2_doubles, h->bar2, h->num_sms};
   c.sw = SvdWork{c.at(L.sW), c.at(L.sJ), c.at(L.sWs), c.at(L.sWh), c.at(L.sTq), c.at(L.sX), c.at(L.sQ), c.at(L.stau),
-                 h->info + 2, h->info, c.pw};
+                 h->info + 2, h->info, c.pw2};
   return c;
 }
 
@@ -198,8 +222,13 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
   if (U) launch_set_identity(st, m, m, U, ldu);
   double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *Wv = c.at(L.Wv), *Tv = c.at(L.Tv), *tauv = c.at(L.tauv);
   double *X = c.at(L.X), *X2 = c.at(L.X2), *Wu = c.at(L.Wu), *Tu = c.at(L.Tu), *tauu = c.at(L.tauu);
-  double *Z1 = c.at(L.Z1), *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp), *Us = c.at(L.Us), *Vs = c.at(L.Vs),
+  double *Z1 = c.at(L.Z1), *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp2), *Us = c.at(L.Us), *Vs = c.at(L.Vs),
          *sig = c.at(L.sig);
+  cudaStream_t sd = c.side;
+  bool svd_pending = false;
+  // the side stream must not start before the work enqueued on the main stream so far
+  UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
+  UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
 
   for (int64_t j0 = 0, step = 0; j0 < n; j0 += b, ++step) {
     const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0, nr = np - bw;
@@ -213,6 +242,7 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
         c.gemm(true, false, np, b, mp, 1.0, Ap, lda, Z, mp, 0.0, Y, np);              // Y = A'^T Z
       }
       panel_qr(st, np, b, Y, np, Wv, np, tauv, Tv, b, c.pw);                          // a3
+      if (svd_pending) UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));             // A12 of step-1
       double* Ac = A + cm(0, j0, lda);                                                 // a4, R1: all rows
       c.gemm(false, false, m, b, np, 1.0, Ac, lda, Wv, np, 0.0, X, m);
       c.gemm(false, false, m, b, b, 1.0, X, m, Tv, b, 0.0, X2, m);
@@ -245,34 +275,43 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
       c.gemm(false, true, m, mp, bw, -1.0, X2, m, Wu, mp, 1.0, Uc, ldu);
     }
     // ---- small SVD and the four updates ----
-    svd_small(st, bw, Ap, lda, Us, b, sig, Vs, b, c.sw);                               // a7
-    launch_set_diag(st, bw, sig, Ap, lda);
+    // a7 on the side stream: it only needs R (this step's panel) and touches A11, A01, A12,
+    // V(:, block), C(block, :), U(:, block).  The next step's sketch, power iterations and
+    // QR(Y) read only the trailing matrix, so they overlap it; the next right update (which
+    // writes A12's rows) waits for ev_svd (reading H5: the updates commute, they must not race).
+    UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
+    UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
+    svd_small(sd, bw, Ap, lda, Us, b, sig, Vs, b, c.sw);                               // a7
+    launch_set_diag(sd, bw, sig, Ap, lda);
     if (j0 > 0) {                                                                       // A01 := A01 V_s
       double* A01 = A + cm(0, j0, lda);
-      c.gemm(false, false, j0, bw, bw, 1.0, A01, lda, Vs, b, 0.0, tmp, j0);
-      launch_copy(st, j0, bw, tmp, j0, A01, lda);
+      c.gemm_side(false, false, j0, bw, bw, 1.0, A01, lda, Vs, b, 0.0, tmp, j0);
+      launch_copy(sd, j0, bw, tmp, j0, A01, lda);
     }
     if (nr > 0) {                                                                       // A12 := U_s^T A12
       double* A12 = A + cm(j0, j0 + bw, lda);
-      c.gemm(true, false, bw, nr, bw, 1.0, Us, b, A12, lda, 0.0, tmp, bw);
-      launch_copy(st, bw, nr, tmp, bw, A12, lda);
+      c.gemm_side(true, false, bw, nr, bw, 1.0, Us, b, A12, lda, 0.0, tmp, bw);
+      launch_copy(sd, bw, nr, tmp, bw, A12, lda);
     }
     if (V) {                                                                            // V1 := V1 V_s
       double* V1 = V + cm(0, j0, ldv);
-      c.gemm(false, false, n, bw, bw, 1.0, V1, ldv, Vs, b, 0.0, tmp, n);
-      launch_copy(st, n, bw, tmp, n, V1, ldv);
+      c.gemm_side(false, false, n, bw, bw, 1.0, V1, ldv, Vs, b, 0.0, tmp, n);
+      launch_copy(sd, n, bw, tmp, n, V1, ldv);
     }
     if (B && k > 0) {                                                                   // C1 := U_s^T C1
       double* C1 = B + cm(j0, 0, ldb);
-      c.gemm(true, false, bw, k, bw, 1.0, Us, b, C1, ldb, 0.0, tmp, bw);
-      launch_copy(st, bw, k, tmp, bw, C1, ldb);
+      c.gemm_side(true, false, bw, k, bw, 1.0, Us, b, C1, ldb, 0.0, tmp, bw);
+      launch_copy(sd, bw, k, tmp, bw, C1, ldb);
     }
     if (U) {                                                                            // U1 := U1 U_s
       double* U1 = U + cm(0, j0, ldu);
-      c.gemm(false, false, m, bw, bw, 1.0, U1, ldu, Us, b, 0.0, tmp, m);
-      launch_copy(st, m, bw, tmp, m, U1, ldu);
+      c.gemm_side(false, false, m, bw, bw, 1.0, U1, ldu, Us, b, 0.0, tmp, m);
+      launch_copy(sd, m, bw, tmp, m, U1, ldu);
     }
+    UTV_CUDA(cudaEventRecord(c.h->ev_svd, sd));
+    svd_pending = true;
   }
+  if (svd_pending) UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
   if (m > n) launch_set_zero(st, m - n, n, A + n, lda);   // rows below T (already 0 by R13; kept explicit)
 }
 
@@ -339,6 +378,13 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
     if (!coop) fail(UTV_ERR_UNSUPPORTED, "device does not support cooperative launch");
     UTV_CUDA(cudaMalloc((void**)&h->bar, 64));
     UTV_CUDA(cudaMemset(h->bar, 0, 64));
+    UTV_CUDA(cudaMalloc((void**)&h->bar2, 64));
+    UTV_CUDA(cudaMemset(h->bar2, 0, 64));
+    int lo = 0, hi = 0;
+    UTV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    UTV_CUDA(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_panel, cudaEventDisableTiming));
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_svd, cudaEventDisableTiming));
     UTV_CUDA(cudaMalloc((void**)&h->info, 64 * sizeof(int)));
     UTV_CUDA(cudaMalloc((void**)&h->flag, sizeof(int)));
     UTV_CUDA(cudaMalloc((void**)&h->d_rank, sizeof(int64_t)));
@@ -359,6 +405,10 @@ utv_status utv_destroy(utv_handle h) {
   if (!h) return UTV_OK;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream); else cudaDeviceSynchronize();
+  if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
+  if (h->ev_panel) cudaEventDestroy(h->ev_panel);
+  if (h->ev_svd) cudaEventDestroy(h->ev_svd);
+  cudaFree(h->bar2);
   cudaFree(h->ws); cudaFree(h->bar); cudaFree(h->info); cudaFree(h->flag); cudaFree(h->d_rank);
   cudaFree(h->vbuf); cudaFree(h->stage);
   cudaFreeHost(h->h_rank); cudaFreeHost(h->h_info);
