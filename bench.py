@@ -225,6 +225,8 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     prof = h.profile_read()
+    if args.profile_dump:
+        h.profile_dump(args.profile_dump)
     h.profile(False)
     clk = clocks.stop()
     t = e0.elapsed_time(e1) / 1e3 / args.steps
@@ -311,6 +313,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=2048)
     ap.add_argument("--ref-n", type=int, default=1536)
+    ap.add_argument("--profile-dump", default="", help="write every timed launch record as CSV (diagnostics)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -73,6 +73,9 @@ typedef struct {
 utv_status utv_profile(utv_handle handle, int enable);
 /* Fill out[0 .. UTV_PROF_FAMILIES-1] from the records so far (synchronises the stream). */
 utv_status utv_profile_read(utv_handle handle, utv_prof_entry* out);
+/* Write every record so far as CSV (family, launches, ms, flops, M, N, K, tag) to `path`
+ * (diagnostics; synchronises). */
+utv_status utv_profile_dump(utv_handle handle, const char* path);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,8 @@ UTV_WANT_V, UTV_WANT_U, UTV_NULLIFY_T12, UTV_HOST_STREAMED = 1, 2, 4, 8
 
 EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "utv_set_stream", "utv_synchronize",
             "utv_factor", "utv_solve", "utv_lstsq", "utv_version", "utv_sketch", "utv_philox", "utv_hqr",
-            "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read"]
+            "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read",
+            "utv_profile_dump"]
 PROF_FAMILIES = ["gemm", "panel", "svd", "sketch", "solve", "misc"]
 
 
@@ -89,6 +90,7 @@ def lib() -> C.CDLL:
             "utv_rank": ([p, i64, p, i64, d, C.POINTER(i64)], st),
             "utv_profile": ([p, C.c_int], st),
             "utv_profile_read": ([p, p], st),
+            "utv_profile_dump": ([p, C.c_char_p], st),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -259,6 +261,9 @@ class Handle:
         self.check(lib().utv_profile_read(self.h, C.cast(arr, C.c_void_p)))
         return {name: {"launches": e.launches, "calls": e.calls, "ms": e.ms, "flops": e.flops, "bytes": e.bytes}
                 for name, e in zip(PROF_FAMILIES, arr)}
+
+    def profile_dump(self, path: str):
+        self.check(lib().utv_profile_dump(self.h, path.encode()))
 
     def rank(self, T, tau: float) -> int:
         r = C.c_int64(0)

@@ -53,20 +53,30 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
 template <int BMN, bool MN_MAJOR>
 constexpr int tile_doubles() { return MN_MAJOR ? BK * (BMN + 8) : BMN * LD_K; }
 
-// Tile configuration: warp tile 64 x 32 (4 x 4 m16n8 fragments), WARPS_N warps along N.
-//   WN = 4: 128 x 128 CTA tile, 256 threads, 1 CTA / SM (long-K products)
-//   WN = 2: 128 x  64 CTA tile, 128 threads, 2 CTAs / SM (short-K updates: one CTA's
-//           epilogue overlaps the other's main loop)
-template <bool TA, bool TB, int WN>
+// Tile configurations (CTA tile M is always 128; warp tile (16 MI) x 32):
+//   0: 2 x 4 warps, MI = 4 -> 128 x 128, 256 threads, 1 CTA / SM (64 accumulators / thread)
+//   1: 2 x 2 warps, MI = 4 -> 128 x  64, 128 threads, 2 CTAs / SM (short K: one CTA's epilogue
+//      overlaps the other's main loop)
+//   2: 4 x 4 warps, MI = 2 -> 128 x 128, 512 threads, 1 CTA / SM (16 warps: more latency hiding)
+//   3: 4 x 2 warps, MI = 2 -> 128 x  64, 256 threads, 2 CTAs / SM
+template <int ID> struct Shape;
+template <> struct Shape<0> { static constexpr int WM = 2, WN = 4, MI = 4, CTAS = 1; };
+template <> struct Shape<1> { static constexpr int WM = 2, WN = 2, MI = 4, CTAS = 2; };
+template <> struct Shape<2> { static constexpr int WM = 4, WN = 4, MI = 2, CTAS = 1; };
+template <> struct Shape<3> { static constexpr int WM = 4, WN = 2, MI = 2, CTAS = 2; };
+
+template <bool TA, bool TB, int ID>
 struct Cfg {
+  static constexpr int WM = Shape<ID>::WM, WN = Shape<ID>::WN, MI = Shape<ID>::MI;
+  static_assert(16 * MI * WM == BM, "CTA tile M must be 128");
   static constexpr int BN = 32 * WN;
-  static constexpr int THREADS = 64 * WN;
+  static constexpr int THREADS = 32 * WM * WN;
   static constexpr bool A_MN = !TA, B_MN = TB;
   static constexpr int A_DBL = tile_doubles<BM, A_MN>();
   static constexpr int B_DBL = tile_doubles<BN, B_MN>();
   static constexpr int STAGE_DBL = A_DBL + B_DBL;
-  static constexpr int CTAS_PER_SM = WN == 4 ? 1 : 2;
-  static constexpr int SMEM_BUDGET = (WN == 4 ? 200 : 110) * 1024;
+  static constexpr int CTAS_PER_SM = Shape<ID>::CTAS;
+  static constexpr int SMEM_BUDGET = (CTAS_PER_SM == 1 ? 200 : 110) * 1024;
   static constexpr int STAGES_FIT = SMEM_BUDGET / (STAGE_DBL * 8);
   static constexpr int STAGES = STAGES_FIT > 4 ? 4 : STAGES_FIT;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_DBL * sizeof(double);
@@ -111,29 +121,39 @@ __device__ __forceinline__ double frag(const double* s, int mn, int k) {
 
 // A operand (m, k): TA=false -> A[m + k lda] (MN-major); TA=true -> A[k + m lda] (K-major).
 // B operand (k, n): TB=false -> B[k + n ldb] (K-major);  TB=true -> B[n + k ldb] (MN-major).
-template <bool TA, bool TB, int VEC, int WN>
-__global__ void __launch_bounds__(Cfg<TA, TB, WN>::THREADS, Cfg<TA, TB, WN>::CTAS_PER_SM)
+template <bool TA, bool TB, int VEC, int ID>
+__global__ void __launch_bounds__(Cfg<TA, TB, ID>::THREADS, Cfg<TA, TB, ID>::CTAS_PER_SM)
 dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
                   const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
                   int64_t k_chunk, double* __restrict__ partial) {
-  using CF = Cfg<TA, TB, WN>;
+  using CF = Cfg<TA, TB, ID>;
   constexpr int BN = CF::BN, THREADS = CF::THREADS, STAGES = CF::STAGES;
+  constexpr int WN = CF::WN, MI = CF::MI, WTM = 16 * MI;   // warp tile WTM x 32
   constexpr bool A_MN = CF::A_MN, B_MN = CF::B_MN;
   extern __shared__ __align__(128) double smem[];
 
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  // Grouped rasterisation: consecutive CTAs walk GROUP_M tile-rows x all tile-columns in
+  // column order, so the CTAs resident at one time share a few MB of A and B rows in L2
+  // (a plain row-major order re-streams the whole B operand from HBM for every tile-row).
+  const int64_t tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  constexpr int64_t GROUP_M = 16;
+  const int64_t pid = blockIdx.x;
+  const int64_t per_group = GROUP_M * tiles_n;
+  const int64_t first_m = (pid / per_group) * GROUP_M;
+  const int64_t gsz = min(tiles_m - first_m, GROUP_M);
+  const int64_t m0 = (first_m + (pid % per_group) % gsz) * BM;
+  const int64_t n0 = ((pid % per_group) / gsz) * BN;
   const int64_t kbeg = (int64_t)blockIdx.z * k_chunk;
   const int64_t kend = min(K, kbeg + k_chunk);
   const int nkt = (int)((kend - kbeg + BK - 1) / BK);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp / WN, wn = warp % WN;      // 2 x WN warps
+  const int wm = warp / WN, wn = warp % WN;      // WM x WN warps
   const int g = lane >> 2, t = lane & 3;
 
-  double acc[4][4][4];
+  double acc[MI][4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -155,11 +175,11 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
   // Software pipeline: the fragments of k-step s+1 are loaded (LDS) while the DMMAs of step s
   // run (register double buffer), and the barrier that publishes the next stage is taken
   // before the last k-step of the current one, so its latency overlaps 16 DMMAs.
-  double af[2][4][2], bf[2][4];
+  double af[2][MI][2], bf[2][4];
   auto load_frags = [&](int buf, const double* sa, const double* sb, int kk) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int mr = wm * 64 + i * 16 + g;
+    for (int i = 0; i < MI; ++i) {
+      const int mr = wm * WTM + i * 16 + g;
       af[buf][i][0] = frag<BM, A_MN>(sa, mr, kk + t);
       af[buf][i][1] = frag<BM, A_MN>(sa, mr + 8, kk + t);
     }
@@ -194,23 +214,23 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
         load_frags(cur ^ 1, sa, sb, (ks + 1) * 4);
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
     }
   }
   cp_async_wait<0>();
 
-  // Epilogue: fragment (i, j): rows m0+wm*64+i*16+g (+8), cols n0+wn*32+j*8+2t (+1).
+  // Epilogue: fragment (i, j): rows m0+wm*WTM+i*16+g (+8), cols n0+wn*32+j*8+2t (+1).
   if (partial) {
     double* P = partial + (size_t)blockIdx.z * (size_t)M * (size_t)N;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int64_t m = m0 + wm * 64 + i * 16 + g + (r >> 1) * 8;
+          const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
           const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
           if (m < M && n < N) P[cm(m, n, M)] = acc[i][j][r];
         }
@@ -218,31 +238,31 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
     if (beta != 0.0) {
       // batch the C loads first (memory-level parallelism), then combine and store
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const int64_t m = m0 + wm * 64 + i * 16 + g + (r >> 1) * 8;
+            const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
             const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
             const double c = (m < M && n < N) ? __ldg(C + cm(m, n, ldc)) : 0.0;
             acc[i][j][r] = alpha * acc[i][j][r] + beta * c;
           }
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] *= alpha;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int64_t m = m0 + wm * 64 + i * 16 + g + (r >> 1) * 8;
+          const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
           const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
           if (m < M && n < N) C[cm(m, n, ldc)] = acc[i][j][r];
         }
@@ -263,69 +283,67 @@ __global__ void dgemm_splitk_reduce(int64_t M, int64_t N, int S, double alpha, c
   }
 }
 
-template <bool TA, bool TB, int VEC, int WN>
+template <bool TA, bool TB, int VEC, int ID>
 void launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splits, int64_t kc,
               double* partial) {
-  using CF = Cfg<TA, TB, WN>;
+  using CF = Cfg<TA, TB, ID>;
   static bool attr_set = false;
-  auto kern = dgemm_dmma_kernel<TA, TB, VEC, WN>;
+  auto kern = dgemm_dmma_kernel<TA, TB, VEC, ID>;
   if (!attr_set) {
     UTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr_set = true;
   }
-  dim3 grid((unsigned)((N + CF::BN - 1) / CF::BN), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
+  dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + BM - 1) / BM)), 1u, (unsigned)splits);
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial);
   UTV_CUDA(cudaGetLastError());
 }
 
-template <int VEC, int WN>
+template <int VEC, int ID>
 void dispatch(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splits,
               int64_t kc, double* partial) {
-  if (!ta && !tb) launch_t<false, false, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else if (ta && !tb) launch_t<true, false, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else if (!ta && tb) launch_t<false, true, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else launch_t<true, true, VEC, WN>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  if (!ta && !tb) launch_t<false, false, VEC, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  else if (ta && !tb) launch_t<true, false, VEC, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  else if (!ta && tb) launch_t<false, true, VEC, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  else launch_t<true, true, VEC, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
 }
 
-int g_force_wn = 0;   // 0 = heuristic; 2 or 4 forces the tile width (benchmarking)
+int g_force_wn = 0;   // 0 = heuristic; 1..3 forces a tile configuration (benchmarking)
 
 }  // namespace
 
-void dgemm_force_tile_width(int wn) { g_force_wn = wn; }
+void dgemm_force_tile_width(int cfg) { g_force_wn = cfg; }
 
-// Launch plan: tile width (WN) and split-K factor from a small cost model (waves of CTAs x
+// Launch plan: tile configuration and split-K factor from a small cost model (waves of CTAs x
 // per-tile time + the split-K reduce traffic).  Fixes wave quantisation: e.g. 782 tiles on 148
 // SMs is 5.28 waves -> 6 (88%); split 3 gives 2346 tiles = 15.85 -> 16 waves (99%).
-struct Plan { int wn; int splits; int64_t kc; };
+struct Plan { int cfg; int splits; int64_t kc; };
+
+int g_cfg_long = 0, g_cfg_short = 1;     // defaults (overridable: UTV_GEMM_CFG_LONG / _SHORT)
 
 static Plan make_plan(int64_t M, int64_t N, int64_t K, int num_sms, size_t work_doubles) {
-  static const int env_wn = [] {
-    const char* e = std::getenv("UTV_GEMM_WN");        // benchmarking override: 2 or 4
-    return e ? std::atoi(e) : 0;
+  static const bool env_read = [] {
+    if (const char* e = std::getenv("UTV_GEMM_CFG_LONG")) g_cfg_long = std::atoi(e) & 3;
+    if (const char* e = std::getenv("UTV_GEMM_CFG_SHORT")) g_cfg_short = std::atoi(e) & 3;
+    return true;
   }();
-  if (!g_force_wn && (env_wn == 2 || env_wn == 4)) g_force_wn = env_wn;
-  Plan best{K <= 1024 ? 2 : 4, 1, K};
-  if (g_force_wn) best.wn = g_force_wn;
+  (void)env_read;
+  const int cfg = g_force_wn ? g_force_wn : (K <= 1024 ? g_cfg_short : g_cfg_long);
+  const int bn = (cfg == 1 || cfg == 3) ? 64 : 128, ctas = (cfg == 1 || cfg == 3) ? 2 : 1;
+  Plan best{cfg, 1, K};
   double best_t = 1e300;
-  for (int wn : {2, 4}) {
-    if (g_force_wn && wn != g_force_wn) continue;
-    if (!g_force_wn && K > 1024 && wn == 2) continue;      // long K: wide tiles (operand reuse)
-    if (!g_force_wn && K <= 1024 && wn == 4) continue;     // short K: 2 CTAs / SM overlap epilogues
-    const int bn = 32 * wn, ctas = wn == 4 ? 1 : 2;
-    const double slots = (double)num_sms * ctas;
-    const double tiles = (double)((M + BM - 1) / BM) * (double)((N + bn - 1) / bn);
-    const double rate = 37.2e12 * 0.85 / slots;            // flop/s per CTA slot
-    for (int s = 1; s <= 128; ++s) {
-      if (s > 1 && (K / s < 256 || (size_t)s * (size_t)M * (size_t)N > work_doubles)) break;
-      const int64_t kc = s == 1 ? K : ((K + s - 1) / s + BK - 1) / BK * BK;
-      const int sp = (int)((K + kc - 1) / kc);
-      const double waves = std::ceil(tiles * sp / slots);
-      double t = waves * (2.0 * BM * bn * (double)kc / rate + 2.5e-6);
-      if (sp > 1) t += 8.0 * (double)M * (double)N * (sp + 1) / 5.0e12 + 4e-6;
-      if (t < best_t * 0.995) { best_t = t; best = Plan{wn, sp, kc}; }
-    }
+  const double slots = (double)num_sms * ctas;
+  const double tiles = (double)((M + BM - 1) / BM) * (double)((N + bn - 1) / bn);
+  const double rate = 37.2e12 * 0.85 / slots;              // flop/s per CTA slot
+  for (int s = 1; s <= 128; ++s) {
+    if (s > 1 && (K / s < 256 || (size_t)s * (size_t)M * (size_t)N > work_doubles)) break;
+    const int64_t kc = s == 1 ? K : ((K + s - 1) / s + BK - 1) / BK * BK;
+    const int sp = (int)((K + kc - 1) / kc);
+    const double waves = std::ceil(tiles * sp / slots);
+    double t = waves * (2.0 * BM * bn * (double)kc / rate + 2.5e-6);
+    if (sp > 1) t += 8.0 * (double)M * (double)N * (sp + 1) / 5.0e12 + 4e-6;
+    if (t < best_t * 0.995) { best_t = t; best = Plan{cfg, sp, kc}; }
   }
   return best;
 }
@@ -359,13 +377,13 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
   double* partial = splits > 1 ? work : nullptr;
   ProfScope prof(st, kProfGemm, splits > 1 ? 2 : 1, 2.0 * (double)M * (double)N * (double)K,
                  8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2.0 : 1.0)));
-  const int wn = plan.wn;
-  if (aligned) {
-    if (wn == 2) dispatch<2, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-    else dispatch<2, 4>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  } else {
-    if (wn == 2) dispatch<1, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-    else dispatch<1, 4>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
+  prof.shape(M, N, K, (ta ? 1 : 0) | (tb ? 2 : 0) | (plan.cfg << 2) | (splits << 8));
+  switch (plan.cfg | (aligned ? 0 : 4)) {
+    case 0: dispatch<2, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    case 1: dispatch<2, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    case 2: dispatch<2, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    case 3: dispatch<2, 3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    default: dispatch<1, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
   }
   if (splits > 1) {
     const int64_t total = M * N;

@@ -1,5 +1,6 @@
 // prof.cu -- see prof.cuh.
 #include "prof.cuh"
+#include <cstdio>
 
 namespace utv {
 
@@ -39,6 +40,29 @@ ProfScope::~ProfScope() {
   ProfRec& r = p->recs[idx];
   r.e1 = p->get();
   if (r.e1) cudaEventRecord(r.e1, st);
+}
+
+void ProfScope::shape(int64_t M, int64_t N, int64_t K, int tag) {
+  Profiler* p = g_prof;
+  if (!rec || !p) return;
+  ProfRec& r = p->recs[idx];
+  r.M = M; r.N = N; r.K = K; r.tag = tag;
+}
+
+long prof_dump(Profiler& p, const char* path) {
+  FILE* f = std::fopen(path, "w");
+  if (!f) return -1;
+  std::fprintf(f, "family,launches,ms,flops,M,N,K,tag\n");
+  long n = 0;
+  for (const ProfRec& r : p.recs) {
+    float ms = 0.f;
+    if (r.e0 && r.e1 && cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) { cudaGetLastError(); ms = -1.f; }
+    std::fprintf(f, "%d,%d,%.6f,%.6e,%lld,%lld,%lld,%d\n", r.family, r.launches, ms, r.flops, (long long)r.M,
+                 (long long)r.N, (long long)r.K, r.tag);
+    ++n;
+  }
+  std::fclose(f);
+  return n;
 }
 
 }  // namespace utv

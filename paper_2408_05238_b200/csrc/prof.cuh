@@ -16,6 +16,8 @@ struct ProfRec {
   int launches;
   double flops, bytes;
   cudaEvent_t e0, e1;
+  int64_t M = 0, N = 0, K = 0;   // GEMM shape (diagnostics)
+  int tag = 0;                   // GEMM: ta | tb << 1 | cfg << 2 | splits << 8
 };
 
 struct Profiler {
@@ -37,6 +39,11 @@ struct ProfScope {
   cudaStream_t st;
   ProfScope(cudaStream_t s, int family, int launches, double flops = 0.0, double bytes = 0.0);
   ~ProfScope();
+  void shape(int64_t M, int64_t N, int64_t K, int tag);
 };
+
+
+// Write every record (family, launches, ms, flops, M, N, K, tag) as CSV; returns records written.
+long prof_dump(Profiler& p, const char* path);
 
 }  // namespace utv

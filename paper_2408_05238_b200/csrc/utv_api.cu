@@ -88,7 +88,7 @@ void ensure_buf(double** p, size_t* have, size_t need) {
 
 // Workspace layout for one factorization (offsets in doubles).
 struct Layout {
-  size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, Tu, tauu, Z1, Z2, tmp, R, Us, Vs, sig;
+  size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, S, Tu, tauu, Z1, Z2, tmp, R, Us, Vs, sig;
   size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve;
   size_t part2, pz1b, pz2b, gram2, px2, gemm2, tmp2;
   size_t gemm_doubles, gemm2_doubles;
@@ -104,12 +104,13 @@ Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
   L.G = take((size_t)m * b);
   L.Y = take((size_t)n * b);
   L.Z = take((size_t)m * b);
-  L.Wv = take((size_t)n * b);
+  L.Wv = take((size_t)n * 2 * b);          // WVZ = [W_V | P'^T]
   L.Tv = take((size_t)b * b);
   L.tauv = take(b);
   L.X = take(mx * b);
   L.X2 = take(mx * b);
-  L.Wu = take((size_t)m * b);
+  L.Wu = take((size_t)m * 2 * b);          // LU = [X2 | W_U]
+  L.S = take((size_t)b * b);
   L.Tu = take((size_t)b * b);
   L.tauu = take(b);
   L.Z1 = take((size_t)b * nk);
@@ -220,8 +221,9 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
   if (B && k > 0) launch_check_finite(st, m, k, B, ldb, c.h->flag);
   if (V) launch_set_identity(st, n, n, V, ldv);
   if (U) launch_set_identity(st, m, m, U, ldu);
-  double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *Wv = c.at(L.Wv), *Tv = c.at(L.Tv), *tauv = c.at(L.tauv);
-  double *X = c.at(L.X), *X2 = c.at(L.X2), *Wu = c.at(L.Wu), *Tu = c.at(L.Tu), *tauu = c.at(L.tauu);
+  double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *WVZ = c.at(L.Wv), *Tv = c.at(L.Tv), *tauv = c.at(L.tauv);
+  double *X = c.at(L.X), *Xv2 = c.at(L.X2), *LU = c.at(L.Wu), *Tu = c.at(L.Tu), *tauu = c.at(L.tauu);
+  double* S = c.at(L.S);
   double *Z1 = c.at(L.Z1), *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp2), *Us = c.at(L.Us), *Vs = c.at(L.Vs),
          *sig = c.at(L.sig);
   cudaStream_t sd = c.side;
@@ -234,45 +236,64 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0, nr = np - bw;
     double* Ap = A + cm(j0, j0, lda);
     // ---- apply transformations from the right ----
-    if (np > b) {  // R5: no sketch for the last block
+    // Fused two-sided update (SURVEY 8(a) a4+a6, K5): the trailing block A_r = A[j0:m, j0+b:n]
+    // gets the right update and the left update in ONE pass with K = 2b,
+    //   A_r -= [X2_r | W_U] [W_r^T ; P'],  P' = T_U^T (W_U^T A_r - (W_U^T X2_r) W_r^T),
+    // exact algebra of  Q_U^T (A_r - X2_r W_r^T)  with X2 = A W_V T_V (R1: all rows) and W_r =
+    // W_V[b:n'].  Only the top rows 0:j0 and the panel block column get a separate K = b update.
+    // LU = [X2 | W_U] (ld m), WVZ = [W_V | P'^T] (ld n').
+    double* X2 = LU;
+    double* Wu = LU + cm(j0, b, m);
+    const bool right = np > b;                        // R5: no sketch for the last block
+    if (right) {
       launch_sketch(st, o.seed, step, j0, mp, b, G, mp, ns);                          // a1
       c.gemm(true, false, np, b, mp, 1.0, Ap, lda, G, mp, 0.0, Y, np);                // Y = A'^T G
       for (int32_t it = 0; it < o.power_iters; ++it) {                                // a2 (R7)
         c.gemm(false, false, mp, b, np, 1.0, Ap, lda, Y, np, 0.0, Z, mp);             // Z = A' Y
         c.gemm(true, false, np, b, mp, 1.0, Ap, lda, Z, mp, 0.0, Y, np);              // Y = A'^T Z
       }
-      panel_qr(st, np, b, Y, np, Wv, np, tauv, Tv, b, c.pw);                          // a3
+      panel_qr(st, np, b, Y, np, WVZ, np, tauv, Tv, b, c.pw);                         // a3: W_V
       if (svd_pending) UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));             // A12 of step-1
       double* Ac = A + cm(0, j0, lda);                                                 // a4, R1: all rows
-      c.gemm(false, false, m, b, np, 1.0, Ac, lda, Wv, np, 0.0, X, m);
-      c.gemm(false, false, m, b, b, 1.0, X, m, Tv, b, 0.0, X2, m);
-      c.gemm(false, true, m, np, b, -1.0, X2, m, Wv, np, 1.0, Ac, lda);
+      c.gemm(false, false, m, b, np, 1.0, Ac, lda, WVZ, np, 0.0, X, m);               // X = A W_V
+      c.gemm(false, false, m, b, b, 1.0, X, m, Tv, b, 0.0, X2, m);                    // X2 = X T_V
+      if (j0 > 0)                                                                      // top rows
+        c.gemm(false, true, j0, np, b, -1.0, X2, m, WVZ, np, 1.0, Ac, lda);
+      c.gemm(false, true, mp, bw, b, -1.0, X2 + j0, m, WVZ, np, 1.0, Ap, lda);       // panel block column
       if (V) {
         double* Vc = V + cm(0, j0, ldv);
-        c.gemm(false, false, n, b, np, 1.0, Vc, ldv, Wv, np, 0.0, X, n);
-        c.gemm(false, false, n, b, b, 1.0, X, n, Tv, b, 0.0, X2, n);
-        c.gemm(false, true, n, np, b, -1.0, X2, n, Wv, np, 1.0, Vc, ldv);
+        c.gemm(false, false, n, b, np, 1.0, Vc, ldv, WVZ, np, 0.0, X, n);
+        c.gemm(false, false, n, b, b, 1.0, X, n, Tv, b, 0.0, Xv2, n);
+        c.gemm(false, true, n, np, b, -1.0, Xv2, n, WVZ, np, 1.0, Vc, ldv);
       }
     }
     // ---- apply transformations from the left ----
-    panel_qr(st, mp, bw, Ap, lda, Wu, mp, tauu, Tu, b, c.pw);                           // a5 (+R13)
+    panel_qr(st, mp, bw, Ap, lda, Wu, m, tauu, Tu, b, c.pw);                            // a5 (+R13)
     if (nr > 0) {                                                                       // a6, R3
       double* Ar = A + cm(j0, j0 + bw, lda);
-      c.gemm(true, false, bw, nr, mp, 1.0, Wu, mp, Ar, lda, 0.0, Z1, bw);
-      c.gemm(true, false, bw, nr, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
-      c.gemm(false, false, mp, nr, bw, -1.0, Wu, mp, Z2, bw, 1.0, Ar, lda);
+      c.gemm(true, false, bw, nr, mp, 1.0, Wu, m, Ar, lda, 0.0, Z1, bw);              // W_U^T A_r
+      if (right) {
+        c.gemm(true, false, bw, b, mp, 1.0, Wu, m, X2 + j0, m, 0.0, S, bw);            // W_U^T X2_r
+        c.gemm(false, true, bw, nr, b, -1.0, S, bw, WVZ + bw, np, 1.0, Z1, bw);      // - S W_r^T
+        // P'^T = Z1^T T_U  into WVZ[bw:n', b:2b]
+        c.gemm(true, false, nr, bw, bw, 1.0, Z1, bw, Tu, b, 0.0, WVZ + cm(bw, b, np), np);
+        c.gemm(false, true, mp, nr, 2 * b, -1.0, X2 + j0, m, WVZ + bw, np, 1.0, Ar, lda);  // fused, K = 2b
+      } else {
+        c.gemm(true, false, bw, nr, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+        c.gemm(false, false, mp, nr, bw, -1.0, Wu, m, Z2, bw, 1.0, Ar, lda);
+      }
     }
     if (B && k > 0) {                                                                   // C := Q_U^T C (v23t)
       double* Cr = B + cm(j0, 0, ldb);
-      c.gemm(true, false, bw, k, mp, 1.0, Wu, mp, Cr, ldb, 0.0, Z1, bw);
+      c.gemm(true, false, bw, k, mp, 1.0, Wu, m, Cr, ldb, 0.0, Z1, bw);
       c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
-      c.gemm(false, false, mp, k, bw, -1.0, Wu, mp, Z2, bw, 1.0, Cr, ldb);
+      c.gemm(false, false, mp, k, bw, -1.0, Wu, m, Z2, bw, 1.0, Cr, ldb);
     }
     if (U) {
       double* Uc = U + cm(0, j0, ldu);
-      c.gemm(false, false, m, bw, mp, 1.0, Uc, ldu, Wu, mp, 0.0, X, m);
-      c.gemm(false, false, m, bw, bw, 1.0, X, m, Tu, b, 0.0, X2, m);
-      c.gemm(false, true, m, mp, bw, -1.0, X2, m, Wu, mp, 1.0, Uc, ldu);
+      c.gemm(false, false, m, bw, mp, 1.0, Uc, ldu, Wu, m, 0.0, X, m);
+      c.gemm(false, false, m, bw, bw, 1.0, X, m, Tu, b, 0.0, Xv2, m);
+      c.gemm(false, true, m, mp, bw, -1.0, Xv2, m, Wu, m, 1.0, Uc, ldu);
     }
     // ---- small SVD and the four updates ----
     // a7 on the side stream: it only needs R (this step's panel) and touches A11, A01, A12,
@@ -576,10 +597,20 @@ utv_status utv_profile(utv_handle h, int enable) {
   });
 }
 
+utv_status utv_profile_dump(utv_handle h, const char* path) {
+  return guarded(h, [&] {
+    if (!path) fail(UTV_ERR_ARG, "path is NULL");
+    UTV_CUDA(cudaStreamSynchronize(h->stream));
+    UTV_CUDA(cudaStreamSynchronize(h->side));
+    if (prof_dump(h->prof, path) < 0) fail(UTV_ERR_ARG, "cannot write the profile file");
+  });
+}
+
 utv_status utv_profile_read(utv_handle h, utv_prof_entry* out) {
   return guarded(h, [&] {
     if (!out) fail(UTV_ERR_ARG, "out is NULL");
     UTV_CUDA(cudaStreamSynchronize(h->stream));
+    UTV_CUDA(cudaStreamSynchronize(h->side));
     for (int f = 0; f < kProfN; ++f) out[f] = utv_prof_entry{0, 0, 0.0, 0.0, 0.0};
     for (const ProfRec& r : h->prof.recs) {
       if (r.family < 0 || r.family >= kProfN) continue;

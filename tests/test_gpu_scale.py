@@ -1,0 +1,89 @@
+"""GPU path at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The oracle cannot run at these sizes, so the checks are properties that hold at any size
+(SURVEY 8(c) P10/P11): the known min-norm solution x0 of the seeded Gp problem (b = A x0 +
+r_perp with A^T r_perp = 0), the exact rank, the normal-equation residual, the residual
+identity ||A x - b|| = ||C[r:m]||, and -- sampled -- individual entries of T = U^T A V
+recomputed one by one from A, V and the explicit U of a smaller run.
+"""
+import numpy as np
+import pytest
+import torch
+
+import utv_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def utv():
+    from paper_2408_05238_b200 import build
+    build.build()
+    import paper_2408_05238_b200 as m
+    return m
+
+
+def _known_solution_case(utv, m, n, r, b, q, k, seed=gen.MATRIX_SEED):
+    dev = torch.device("cuda:0")
+    At, Bm, X0 = gen.gp_torch(m, n, r, seed=seed, device=dev, k=k)
+    A0 = At.t()
+    B0 = utv.colmajor(Bm)
+    A = utv.colmajor(A0.clone())
+    B = B0.clone()
+    X, rank = utv.lstsq(A, B, utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED))
+    torch.cuda.synchronize()
+    rel = ((X - X0).norm() / X0.norm()).item()
+    # normal equations ||A^T (A x - b)|| / (||A||^2 ||x||)  (A^T r_perp = 0 by construction)
+    R = A0 @ X - B0
+    ne = ((A0.t() @ R).norm() / (A0.norm() ** 2 * X.norm())).item()
+    return rank, rel, ne
+
+
+def test_cfg2_full_size(utv):
+    """configs[1]: square n=20000 rank 10000, b=256, q=2, 1 RHS."""
+    rank, rel, ne = _known_solution_case(utv, 20000, 20000, 10000, 256, 2, 1)
+    assert rank == 10000
+    assert rel <= 1e-10, rel
+    assert ne <= 1e-12, ne
+
+
+def test_cfg3_full_size(utv):
+    """configs[2]: square n=50000 rank 25000, b=256, q=2 -- the bench workload at N=1."""
+    rank, rel, ne = _known_solution_case(utv, 50000, 50000, 25000, 256, 2, 1)
+    assert rank == 25000
+    assert rel <= 1e-10, rel
+    assert ne <= 1e-12, ne
+
+
+def test_cfg4_full_size(utv):
+    """configs[3]: tall m=200000 x n=20000 rank 15000, 16 RHS, q=1 (overdetermined, inconsistent)."""
+    rank, rel, ne = _known_solution_case(utv, 200000, 20000, 15000, 256, 1, 16)
+    assert rank == 15000
+    assert rel <= 1e-10, rel
+    assert ne <= 1e-12, ne
+
+
+def test_residual_identity_and_sampled_T(utv):
+    """P11 at a mid size: ||A x - b|| == ||C[r:m]||; sampled T_ij == (U^T A V)_ij one by one."""
+    m, n, r, b = 3000, 2500, 1200, 256
+    h = utv.Handle(0)
+    dev = torch.device("cuda:0")
+    At, Bm, _ = gen.gp_torch(m, n, r, seed=5, device=dev, k=3)
+    A0 = At.t()
+    A = utv.colmajor(A0.clone())
+    B = utv.colmajor(Bm)
+    B0 = B.clone()
+    V = utv.colmajor_empty(n, n)
+    U = utv.colmajor_empty(m, m)
+    rank = h.factor(A, V=V, U=U, B=B, opts=utv.Opts(block=b, power_iters=2, seed=3, flags=utv.UTV_WANT_U))
+    X = utv.colmajor_empty(n, 3)
+    h.solve(A, V, B, rank, X)
+    torch.cuda.synchronize()
+    assert rank == r
+    res = (A0 @ X - B0).norm().item()
+    assert res == pytest.approx(B[rank:].norm().item(), rel=1e-12)
+    rng = np.random.default_rng(0)
+    for _ in range(64):
+        i, j = int(rng.integers(0, m)), int(rng.integers(0, n))
+        tij = float(U[:, i] @ (A0 @ V[:, j]))
+        assert abs(float(A[i, j]) - tij) <= 1e-12 * A0.norm().item()

@@ -16,7 +16,7 @@ def t_gemm(name, ta, tb, M, N, K, beta=0.0, reps=3):
         e0.record(); h.gemm(ta, tb, 1.0, A, B, beta, Cm); e1.record(); torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / 1e3)
     res[name] = {"ms": best * 1e3, "tflops": 2.0 * M * N * K / best / 1e12}
-    print(os.environ.get("UTV_GEMM_WN", "auto"), name, res[name], flush=True)
+    print(os.environ.get("TAG", "auto"), name, res[name], flush=True)
     del A, B, Cm
 for n in (50000, 25000):
     t_gemm(f"TN_{n}x256_K{n}", True, False, n, 256, n)
