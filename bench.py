@@ -311,7 +311,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-n", type=int, default=2048)
+    ap.add_argument("--cpu-n", type=int, default=3072)
     ap.add_argument("--ref-n", type=int, default=1536)
     ap.add_argument("--profile-dump", default="", help="write every timed launch record as CSV (diagnostics)")
     args = ap.parse_args()
