@@ -38,6 +38,21 @@ utv_status utv_hqr(utv_handle handle, int64_t m, int64_t w, double* P, int64_t l
 utv_status utv_svd_small(utv_handle handle, int64_t b, const double* R, int64_t ldr, double* Us,
                          int64_t ldu, double* sigma, double* Vs, int64_t ldv, int32_t* sweeps);
 
+/* a7 in place -- "[A11, U_SVD, V_SVD] := SVD(A11)": the b x b upper-triangular block
+ * A11 (lda) is replaced by diag(sigma); U_s, V_s, sigma as utv_svd_small.  Asynchronous: a
+ * Jacobi failure is recorded in the handle and reported by utv_svd_status. */
+utv_status utv_svd_block(utv_handle handle, int64_t b, double* A11, int64_t lda, double* Us,
+                         int64_t ldu, double* sigma, double* Vs, int64_t ldv);
+
+/* Read (and clear) the Jacobi status accumulated by utv_svd_block calls: *failed != 0 if any
+ * block exceeded 30 sweeps; *max_sweeps the largest sweep count (synchronises). */
+utv_status utv_svd_status(utv_handle handle, int32_t* failed, int32_t* max_sweeps);
+
+/* a9 -- Z (n x k, ldz) := T(0:n, 0:n)^{-1} Z for upper-triangular T (ldt) (back substitution of
+ * eq:simplesoln P:894-901 in 256-row blocks: block solve + DMMA GEMM updates). */
+utv_status utv_trsm_upper(utv_handle handle, int64_t n, const double* T, int64_t ldt, double* Z,
+                          int64_t ldz, int64_t k);
+
 /* a2 / a4 / a6 primitive -- FP64 DMMA GEMM: C = alpha op(A) op(B) + beta C, op = transpose
  * when ta / tb != 0 (C is not read when beta == 0). */
 utv_status utv_gemm(utv_handle handle, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha,
@@ -47,6 +62,10 @@ utv_status utv_gemm(utv_handle handle, int ta, int tb, int64_t M, int64_t N, int
 /* a8 -- Compute_rank (R10) of T's diagonal (n entries); synchronises. */
 utv_status utv_rank(utv_handle handle, int64_t n, const double* T, int64_t ldt, double tau,
                     int64_t* rank);
+
+/* a8 on a vector: the same rule for the n diagonal entries d[0..n-1] gathered contiguously
+ * (multi-GPU path, where diag(T) is spread over the column owners); synchronises. */
+utv_status utv_rank_diag(utv_handle handle, int64_t n, const double* d, double tau, int64_t* rank);
 
 /* ---- instrumentation (bench.py) -----------------------------------------------------
  * When enabled, every kernel launch of the library on this handle is bracketed by CUDA events

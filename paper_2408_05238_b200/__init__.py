@@ -26,7 +26,8 @@ UTV_WANT_V, UTV_WANT_U, UTV_NULLIFY_T12, UTV_HOST_STREAMED = 1, 2, 4, 8
 EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "utv_set_stream", "utv_synchronize",
             "utv_factor", "utv_solve", "utv_lstsq", "utv_version", "utv_sketch", "utv_philox", "utv_hqr",
             "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read",
-            "utv_profile_dump"]
+            "utv_profile_dump", "utv_svd_block", "utv_svd_status", "utv_trsm_upper",
+            "utv_rank_diag"]
 PROF_FAMILIES = ["gemm", "panel", "svd", "sketch", "solve", "misc"]
 
 
@@ -91,6 +92,10 @@ def lib() -> C.CDLL:
             "utv_profile": ([p, C.c_int], st),
             "utv_profile_read": ([p, p], st),
             "utv_profile_dump": ([p, C.c_char_p], st),
+            "utv_svd_block": ([p, i64, p, i64, p, i64, p, p, i64], st),
+            "utv_svd_status": ([p, C.POINTER(i32), C.POINTER(i32)], st),
+            "utv_trsm_upper": ([p, i64, p, i64, p, i64, i64], st),
+            "utv_rank_diag": ([p, i64, p, d, C.POINTER(i64)], st),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -245,6 +250,30 @@ class Handle:
                                        C.byref(sw)))
         return Us, s, Vs, int(sw.value)
 
+    def svd_block(self, A11, Us=None, s=None, Vs=None):
+        """A11 (b x b upper triangular, in place) := diag(sigma); returns (U_s, sigma, V_s)."""
+        _check_f64(A11)
+        b = A11.shape[0]
+        dev = A11.device
+        Us = colmajor_empty(b, b, device=dev) if Us is None else Us
+        Vs = colmajor_empty(b, b, device=dev) if Vs is None else Vs
+        s = torch.empty(b, dtype=torch.float64, device=dev) if s is None else s
+        self.check(lib().utv_svd_block(self.h, b, _ptr(A11), _ld(A11), _ptr(Us), _ld(Us), _ptr(s), _ptr(Vs), _ld(Vs)))
+        return Us, s, Vs
+
+    def svd_status(self):
+        f, sw = C.c_int32(0), C.c_int32(0)
+        self.check(lib().utv_svd_status(self.h, C.byref(f), C.byref(sw)))
+        return int(f.value), int(sw.value)
+
+    def trsm_upper(self, T, Z):
+        """Z := T^{-1} Z for the leading Z.shape[0] x Z.shape[0] block of upper-triangular T."""
+        _check_f64(T, Z)
+        n = Z.shape[0]
+        k = Z.shape[1] if Z.dim() == 2 else 1
+        self.check(lib().utv_trsm_upper(self.h, n, _ptr(T), _ld(T), _ptr(Z), _ld(Z), k))
+        return Z
+
     def gemm(self, ta: bool, tb: bool, alpha: float, A, B, beta: float, Cm):
         _check_f64(A, B, Cm)
         M, N = Cm.shape
@@ -264,6 +293,11 @@ class Handle:
 
     def profile_dump(self, path: str):
         self.check(lib().utv_profile_dump(self.h, path.encode()))
+
+    def rank_diag(self, d, tau: float) -> int:
+        r = C.c_int64(0)
+        self.check(lib().utv_rank_diag(self.h, d.numel(), _ptr(d), float(tau), C.byref(r)))
+        return int(r.value)
 
     def rank(self, T, tau: float) -> int:
         r = C.c_int64(0)

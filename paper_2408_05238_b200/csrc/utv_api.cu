@@ -563,6 +563,45 @@ utv_status utv_svd_small(utv_handle h, int64_t b, const double* R, int64_t ldr, 
   });
 }
 
+utv_status utv_svd_block(utv_handle h, int64_t b, double* A11, int64_t lda, double* Us, int64_t ldu, double* sigma,
+                         double* Vs, int64_t ldv) {
+  return guarded(h, [&] {
+    if (b < 1) fail(UTV_ERR_ARG, "b < 1");
+    if (b > 256) fail(UTV_ERR_UNSUPPORTED, "b > 256");
+    if (!A11 || !Us || !sigma || !Vs) fail(UTV_ERR_ARG, "NULL pointer");
+    check_ld("lda", lda, b); check_ld("ldu", ldu, b); check_ld("ldv", ldv, b);
+    Ctx c = make_ctx(h, b, b, 1, b);
+    svd_small(h->stream, b, A11, lda, Us, ldu, sigma, Vs, ldv, c.sw);   // info accumulates (sticky)
+    launch_set_diag(h->stream, b, sigma, A11, lda);                    // A11 := Sigma
+  });
+}
+
+utv_status utv_svd_status(utv_handle h, int32_t* failed, int32_t* max_sweeps) {
+  return guarded(h, [&] {
+    UTV_CUDA(cudaMemcpyAsync(h->h_info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    UTV_CUDA(cudaStreamSynchronize(h->stream));
+    if (max_sweeps) *max_sweeps = h->h_info[0];
+    if (failed) *failed = h->h_info[1];
+    UTV_CUDA(cudaMemsetAsync(h->info, 0, 2 * sizeof(int), h->stream));
+  });
+}
+
+utv_status utv_trsm_upper(utv_handle h, int64_t n, const double* T, int64_t ldt, double* Z, int64_t ldz, int64_t k) {
+  return guarded(h, [&] {
+    if (n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
+    if (n == 0 || k == 0) return;
+    if (!T || !Z) fail(UTV_ERR_ARG, "NULL pointer");
+    check_ld("ldt", ldt, n); check_ld("ldz", ldz, n);
+    Ctx c = make_ctx(h, n, n, k, 1);
+    constexpr int64_t SB = 256;
+    for (int64_t j0 = ((n - 1) / SB) * SB; j0 >= 0; j0 -= SB) {
+      const int64_t j1 = std::min(n, j0 + SB);
+      launch_trsv_block(c.st, j0, j1, T, ldt, Z, ldz, k);
+      if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Z + j0, ldz, 1.0, Z, ldz);
+    }
+  });
+}
+
 utv_status utv_gemm(utv_handle h, int ta, int tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                     int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
   return guarded(h, [&] {
@@ -574,6 +613,19 @@ utv_status utv_gemm(utv_handle h, int ta, int tb, int64_t M, int64_t N, int64_t 
     if (need) ensure_buf(&h->ws, &h->ws_doubles, need);
     dgemm(h->stream, ta != 0, tb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h->ws, h->ws_doubles,
           h->num_sms);
+  });
+}
+
+utv_status utv_rank_diag(utv_handle h, int64_t n, const double* d, double tau, int64_t* rank) {
+  return guarded(h, [&] {
+    if (n < 0 || !rank) fail(UTV_ERR_ARG, "bad argument");
+    if (!(tau >= 0.0 && tau < 1.0)) fail(UTV_ERR_ARG, "tau not in [0, 1)");
+    if (n == 0) { *rank = 0; return; }
+    if (!d) fail(UTV_ERR_ARG, "d is NULL");
+    launch_rank(h->stream, n, d, 0, tau, h->d_rank);     // ldt = 0: T[j + j*0] = d[j]
+    UTV_CUDA(cudaMemcpyAsync(h->h_rank, h->d_rank, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    UTV_CUDA(cudaStreamSynchronize(h->stream));
+    *rank = *h->h_rank;
   });
 }
 
