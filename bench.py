@@ -6,12 +6,12 @@ n=50000 @1/2/4/8".  One step = one full utv_lstsq (factor + rank + solve, all SU
 rows) on a fresh copy of the synthetic cfg3 problem (square n = 50000, rank 25000, b = 256,
 q = 2, 1 RHS; the paper's generator P:2436-2448, known min-norm solution).  `value` is the
 ALGORITHMIC FP64 rate F_alg / time (SURVEY App. B flop model, implementation independent),
-summed over ranks.  Inputs (20 GB) are far larger than the 126 MB L2, so no flush is needed.
+for the whole job.  Inputs (20 GB) are far larger than the 126 MB L2, so no flush is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
 
-N > 1 (torchrun): every rank solves its own cfg3 instance (replicas, weak scaling, no data-path
-collective): the block-column-sharded strong-scaling path of SURVEY 8(e) is not built yet.
+N > 1 (torchrun): ONE cfg3 problem on all ranks (strong scaling): block-cyclic columns, NCCL
+AllReduce / AllGather / Broadcast per step (paper_2408_05238_b200.dist).
 `--impl reference`: the CPU oracle (oracle/, the only comparison program that exists for this
 paper) timed on the host cores on a bounded sample of the same recipe.
 """
@@ -166,7 +166,7 @@ def run_reference(args):
     val = F / t / 1e12
     out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"{args.config} recipe, bounded CPU sample n={n_s}", "sample_n": n_s},
            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": oracle.get_threads(), "kind": "oracle",
                             "sample": f"oracle lstsq, cfg3 recipe at n={n_s} (rank {n_s // 2}, b=256, q=2)"},
@@ -189,24 +189,43 @@ def run_ours(args):
 
     m, n, r_true, b, q, k = CONFIGS[args.config]
     opts = utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED)
-    # synthetic cfg instance, one per rank (different seeds), column-major on the device
-    At, Bm, X0 = gen.gp_torch(m, n, r_true, seed=gen.MATRIX_SEED + rank, device=dev, k=k)
+    # one synthetic cfg instance (same seed on every rank), column-major on the device
+    At, Bm, X0 = gen.gp_torch(m, n, r_true, seed=gen.MATRIX_SEED, device=dev, k=k)
     A0 = At.t()                                   # pristine copy, column-major m x n
     B0 = utv.colmajor(Bm)
-    A = utv.colmajor_empty(m, n, device=dev)
-    B = utv.colmajor_empty(m, k, device=dev)
-    X = utv.colmajor_empty(n, k, device=dev)
     h = utv.Handle(dev.index)
     stream = h.stream
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
+        # strong scaling: the block-cyclic multi-GPU path solves ONE problem
+        from paper_2408_05238_b200 import dist as D
+        A0 = D.scatter_columns(A0, b, world, rank)   # this rank's pristine shard
+        del At
+        torch.cuda.empty_cache()
+        A = utv.colmajor_empty(m, A0.shape[1], device=dev)
+        steps_backend = D.CudaSteps(h)
+        Xbox = [None]
 
-    def step():
-        A.copy_(A0)
-        B.copy_(B0)
-        return h.lstsq(A, B, X, opts)
+        def step():
+            A.copy_(A0)
+            Xd, rr = D.lstsq_dist(A, B0, n, b=b, q=q, tau=opts.tau, seed=opts.seed, steps=steps_backend)
+            Xbox[0] = Xd
+            return rr
+    else:
+        A = utv.colmajor_empty(m, n, device=dev)
+        B = utv.colmajor_empty(m, k, device=dev)
+        Xs = utv.colmajor_empty(n, k, device=dev)
+        Xbox = [Xs]
+
+        def step():
+            A.copy_(A0)
+            B.copy_(B0)
+            return h.lstsq(A, B, Xs, opts)
 
     for _ in range(args.warmup):
         r = step()
     torch.cuda.synchronize()
+    X = Xbox[0]
     rel_err = float(((X - X0).norm() / X0.norm()).item())
 
     clocks = ClockSampler(dev.index)
@@ -235,11 +254,36 @@ def run_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t = float(tt.item())
     F = f_alg(m, n, b, q, k, r)
-    value = world * F / t / 1e12
+    value = F / t / 1e12                          # one problem on all ranks (strong scaling)
 
     # ---- end-to-end through the C ABI with HOST buffers (H2D of A, B and D2H of X inside) ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and use_dist:
+        # multi-GPU: pinned host shard -> device, lstsq_dist, X -> host, all inside the timed region
+        Ah = torch.empty(A0.t().shape, dtype=torch.float64, pin_memory=True).t()
+        Ah.copy_(A0)
+        Bh = torch.empty(B0.t().shape, dtype=torch.float64, pin_memory=True).t()
+        Bh.copy_(B0)
+        Bd = utv.colmajor_empty(m, k, device=dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        A.copy_(Ah, non_blocking=True)
+        Bd.copy_(Bh, non_blocking=True)
+        Xd, re = D.lstsq_dist(A, Bd, n, b=b, q=q, tau=opts.tau, seed=opts.seed, steps=steps_backend)
+        Xh = Xd.cpu()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / 1e3
+        if world > 1:
+            tt = torch.tensor([te], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": F / te / 1e12, "unit": "TFLOP/s", "seconds": te,
+               "h2d_bytes_per_step": 8 * (m * n + world * m * k), "d2h_bytes_per_step": 8 * world * n * k,
+               "steps": 1, "rank_ok": re == r}
+    elif not args.no_e2e:
         Ah = utv.colmajor_empty(m, n, device="cpu", pin_memory=True)
         Ah.copy_(A0)
         Bh = utv.colmajor_empty(m, k, device="cpu", pin_memory=True)
@@ -258,7 +302,7 @@ def run_ours(args):
             tt = torch.tensor([te], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             te = float(tt.item())
-        e2e = {"value": world * F / te / 1e12, "unit": "TFLOP/s", "seconds": te,
+        e2e = {"value": F / te / 1e12, "unit": "TFLOP/s", "seconds": te,
                "h2d_bytes_per_step": 8 * (m * n + m * k), "d2h_bytes_per_step": 8 * n * k, "steps": 1,
                "rank_ok": re == r}
         del Ah, Bh, Xh
@@ -275,12 +319,15 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "time_to_solution_s": t, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: square n={n} rank {r_true}, b={b}, q={q}, k={k} (paper generator "
                                "P:2436-2448, known min-norm solution)", "m": m, "n": n, "rank": r_true, "block": b,
-                   "power_iters": q, "rhs": k, "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "power_iters": q, "rhs": k,
+                   "parallelism": f"blockcyclic{world}" if use_dist else "single",
                    "l2": "inputs (8mn = %.1f GB) >> 126 MB L2; no flush needed" % (8 * m * n / 1e9),
-                   "step": "restore A,B from a pristine device copy (D2D) + utv_lstsq"},
+                   "step": ("restore the rank's A shard from a pristine device copy (D2D) + lstsq_dist "
+                            "(block-cyclic columns, NCCL)") if use_dist else
+                           "restore A,B from a pristine device copy (D2D) + utv_lstsq"},
         "frac_of_fp64_peak": value / (world * peak),
         "fp64_peak_tflops": peak, "f_alg": F, "rank": r, "rank_ok": r == r_true, "rel_err_x0": rel_err,
         "roofline": {"kernel": "dgemm_dmma_kernel (FP64 mma.sync DMMA, all GEMM launches of the step)",
@@ -313,6 +360,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=3072)
     ap.add_argument("--ref-n", type=int, default=1536)
+    ap.add_argument("--force-dist", action="store_true", help="use the multi-GPU (block-cyclic) path even at N=1")
     ap.add_argument("--profile-dump", default="", help="write every timed launch record as CSV (diagnostics)")
     args = ap.parse_args()
     if args.impl == "reference":
