@@ -44,7 +44,8 @@ enum {
   UTV_WANT_V = 1u,           /* (informational: V is produced whenever a V pointer is passed) */
   UTV_WANT_U = 2u,           /* build U explicitly (v21t semantics) when U != NULL */
   UTV_NULLIFY_T12 = 4u,      /* reserved (NEXT): Nullify_top_right_part_of_T, fig:alg_nullify_t12 */
-  UTV_HOST_STREAMED = 8u     /* reserved (NEXT): out-of-core streaming from pinned host memory */
+  UTV_HOST_STREAMED = 8u,    /* reserved (NEXT): out-of-core streaming from pinned host memory */
+  UTV_EXPLICIT_V = 16u       /* utv_lstsq: accumulate V explicitly (default: factored V, see below) */
 };
 
 /* Parameters of randUTV(A, q, n_b) (fig:alg_utv) and Compute_rank. */
@@ -106,8 +107,10 @@ utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const d
 /*
  * Solve_linear_system, fast option (fig:alg_axb P:1075-1108 without the Nullify line;
  * "Fast option" P:1114-1121; v34s): factor + Compute_rank + solve.  A and B are consumed
- * (overwritten by T and U^T B); X (n x k) written; *rank = r.  V is kept in the handle's
- * workspace.  A, B and X may be HOST pointers (pageable or pinned): they are then staged
+ * (overwritten by T and U^T B); X (n x k) written; *rank = r.  V is not formed: the handle keeps
+ * every step's block reflector (W_V, T_V) and V_s (about n^2/2 doubles instead of n^2) and
+ * applies V = Q_1 ... Q_s blockdiag(V_s) to [z; 0] (saves the 2 n^3 flops of
+ * accumulating V); opts->flags & UTV_EXPLICIT_V accumulates V explicitly instead.  A, B and X may be HOST pointers (pageable or pinned): they are then staged
  * through device buffers inside the call (the end-to-end path); host A and B are inputs only
  * (left unchanged), a host X is written and the call returns after X has landed.
  */

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libutv.so")
 
 UTV_OK, UTV_ERR_ARG, UTV_ERR_SHAPE, UTV_ERR_ALLOC, UTV_ERR_CUDA = 0, -1, -2, -3, -4
 UTV_ERR_NCCL, UTV_ERR_NUMERICAL, UTV_ERR_UNSUPPORTED = -5, -6, -7
-UTV_WANT_V, UTV_WANT_U, UTV_NULLIFY_T12, UTV_HOST_STREAMED = 1, 2, 4, 8
+UTV_WANT_V, UTV_WANT_U, UTV_NULLIFY_T12, UTV_HOST_STREAMED, UTV_EXPLICIT_V = 1, 2, 4, 8, 16
 
 EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "utv_set_stream", "utv_synchronize",
             "utv_factor", "utv_solve", "utv_lstsq", "utv_version", "utv_sketch", "utv_philox", "utv_hqr",

@@ -208,9 +208,29 @@ void copy2d(cudaStream_t st, void* dst, int64_t ldd, const void* src, int64_t ld
   UTV_CUDA(cudaMemcpy2DAsync(dst, (size_t)ldd * 8, src, (size_t)lds * 8, (size_t)rows * 8, (size_t)cols, kind, st));
 }
 
+// Factored V: instead of accumulating V explicitly (2 n^3 flops at square
+// shapes, 23% of the work at q = 2), keep every step's block reflector (W_V, T_V) and V_s:
+//   V = Q_1 Q_2 ... Q_s D_1 ... D_s   (D_i = V_s on block i commutes with Q_j, j > i: H5),
+// and apply it to [z; 0] in the solve.  Used by utv_lstsq (V is not an output there).
+struct FactoredV {
+  double* W;       // sum_i n'_i b doubles: W_V of step i at woff[i] (ld n'_i)
+  double* T;       // nsteps b^2: T_V of step i (ld b)
+  double* Vs;      // nsteps b^2: V_s of step i (ld b)
+  std::vector<size_t> woff;
+  std::vector<int64_t> j0, np;
+  std::vector<char> has_q;
+};
+
+size_t factored_w_doubles(int64_t n, int64_t b) {
+  size_t tot = 0;
+  for (int64_t j0 = 0; j0 < n; j0 += b)
+    if (n - j0 > b) tot += (size_t)(n - j0) * b;
+  return tot;
+}
+
 // The randUTV factorization on device buffers (fig:alg_utv).
 void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, double* V, int64_t ldv, double* U,
-                 int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts& o) {
+                 int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts& o, FactoredV* fv = nullptr) {
   cudaStream_t st = c.st;
   const Layout& L = c.L;
   const int64_t b = o.block;
@@ -252,18 +272,24 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
         c.gemm(false, false, mp, b, np, 1.0, Ap, lda, Y, np, 0.0, Z, mp);             // Z = A' Y
         c.gemm(true, false, np, b, mp, 1.0, Ap, lda, Z, mp, 0.0, Y, np);              // Y = A'^T Z
       }
-      panel_qr(st, np, b, Y, np, WVZ, np, tauv, Tv, b, c.pw);                         // a3: W_V
+      double* Tvs = fv ? fv->T + (size_t)step * b * b : Tv;                            // T_V (kept if factored)
+      panel_qr(st, np, b, Y, np, WVZ, np, tauv, Tvs, b, c.pw);                        // a3: W_V
+      if (fv) {
+        fv->woff.push_back(fv->woff.empty() ? 0 : fv->woff.back() + (size_t)fv->np.back() * b);
+        fv->j0.push_back(j0); fv->np.push_back(np); fv->has_q.push_back(1);
+        launch_copy(st, np, b, WVZ, np, fv->W + fv->woff.back(), np);
+      }
       if (svd_pending) UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));             // A12 of step-1
       double* Ac = A + cm(0, j0, lda);                                                 // a4, R1: all rows
       c.gemm(false, false, m, b, np, 1.0, Ac, lda, WVZ, np, 0.0, X, m);               // X = A W_V
-      c.gemm(false, false, m, b, b, 1.0, X, m, Tv, b, 0.0, X2, m);                    // X2 = X T_V
+      c.gemm(false, false, m, b, b, 1.0, X, m, Tvs, b, 0.0, X2, m);                   // X2 = X T_V
       if (j0 > 0)                                                                      // top rows
         c.gemm(false, true, j0, np, b, -1.0, X2, m, WVZ, np, 1.0, Ac, lda);
       c.gemm(false, true, mp, bw, b, -1.0, X2 + j0, m, WVZ, np, 1.0, Ap, lda);       // panel block column
       if (V) {
         double* Vc = V + cm(0, j0, ldv);
         c.gemm(false, false, n, b, np, 1.0, Vc, ldv, WVZ, np, 0.0, X, n);
-        c.gemm(false, false, n, b, b, 1.0, X, n, Tv, b, 0.0, Xv2, n);
+        c.gemm(false, false, n, b, b, 1.0, X, n, Tvs, b, 0.0, Xv2, n);
         c.gemm(false, true, n, np, b, -1.0, Xv2, n, WVZ, np, 1.0, Vc, ldv);
       }
     }
@@ -302,11 +328,12 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     // writes A12's rows) waits for ev_svd (reading H5: the updates commute, they must not race).
     UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
     UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
-    svd_small(sd, bw, Ap, lda, Us, b, sig, Vs, b, c.sw);                               // a7
+    double* Vsi = fv ? fv->Vs + (size_t)step * b * b : Vs;                             // V_s (kept if factored)
+    svd_small(sd, bw, Ap, lda, Us, b, sig, Vsi, b, c.sw);                              // a7
     launch_set_diag(sd, bw, sig, Ap, lda);
     if (j0 > 0) {                                                                       // A01 := A01 V_s
       double* A01 = A + cm(0, j0, lda);
-      c.gemm_side(false, false, j0, bw, bw, 1.0, A01, lda, Vs, b, 0.0, tmp, j0);
+      c.gemm_side(false, false, j0, bw, bw, 1.0, A01, lda, Vsi, b, 0.0, tmp, j0);
       launch_copy(sd, j0, bw, tmp, j0, A01, lda);
     }
     if (nr > 0) {                                                                       // A12 := U_s^T A12
@@ -316,7 +343,7 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     }
     if (V) {                                                                            // V1 := V1 V_s
       double* V1 = V + cm(0, j0, ldv);
-      c.gemm_side(false, false, n, bw, bw, 1.0, V1, ldv, Vs, b, 0.0, tmp, n);
+      c.gemm_side(false, false, n, bw, bw, 1.0, V1, ldv, Vsi, b, 0.0, tmp, n);
       launch_copy(sd, n, bw, tmp, n, V1, ldv);
     }
     if (B && k > 0) {                                                                   // C1 := U_s^T C1
@@ -366,6 +393,36 @@ void solve_impl(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t ldt
     if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Zb + j0, r, 1.0, Zb, r);
   }
   c.gemm(false, false, n, k, r, 1.0, V, ldv, Zb, r, 0.0, X, ldx);
+}
+
+// X = V(:, 0:r) z with V in factored form: X = Q_1 ... Q_s D [z; 0]  (X is n x k, ldx).
+void solve_factored(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t ldt, const double* Cm, int64_t ldc,
+                    int64_t k, double* X, int64_t ldx, const FactoredV& fv, int64_t b) {
+  cudaStream_t st = c.st;
+  if (k <= 0) return;
+  launch_set_zero(st, n, k, X, ldx);
+  if (r <= 0) return;
+  double* Zb = c.at(c.L.zsolve);
+  launch_copy(st, r, k, Cm, ldc, Zb, r);
+  constexpr int64_t SB = 256;
+  for (int64_t j0 = ((r - 1) / SB) * SB; j0 >= 0; j0 -= SB) {                 // z = T11^{-1} C(0:r)
+    const int64_t j1 = std::min(r, j0 + SB);
+    launch_trsv_block(st, j0, j1, T, ldt, Zb, r, k);
+    if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Zb + j0, r, 1.0, Zb, r);
+  }
+  double* tmp = c.at(c.L.Z1);
+  double* tmp2 = c.at(c.L.Z2);
+  for (int64_t j0 = 0, step = 0; j0 < r; j0 += b, ++step) {                  // D: X(blk) = V_s,i z(blk)
+    const int64_t bw = std::min(b, n - j0), zr = std::min(bw, r - j0);
+    c.gemm(false, false, bw, k, zr, 1.0, fv.Vs + (size_t)step * b * b, b, Zb + j0, r, 0.0, X + j0, ldx);
+  }
+  for (int64_t i = (int64_t)fv.woff.size() - 1; i >= 0; --i) {                // X = Q_i X, i = s..1
+    const int64_t j0 = fv.j0[i], np = fv.np[i];
+    const double* W = fv.W + fv.woff[i];
+    c.gemm(true, false, b, k, np, 1.0, W, np, X + j0, ldx, 0.0, tmp, b);
+    c.gemm(false, false, b, k, b, 1.0, fv.T + (size_t)(j0 / b) * b * b, b, tmp, b, 0.0, tmp2, b);
+    c.gemm(false, false, np, k, b, -1.0, W, np, tmp2, b, 1.0, X + j0, ldx);
+  }
 }
 
 bool is_device_ptr(const void* p) {
@@ -503,11 +560,27 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     if (hA) { dA = h->stage + off; dlda = m; off += (size_t)m * n; copy2d(st, dA, m, A, lda, m, n, cudaMemcpyHostToDevice); }
     if (hB) { dB = h->stage + off; dldb = m; off += (size_t)m * k; copy2d(st, dB, m, B, ldb, m, k, cudaMemcpyHostToDevice); }
     if (hX) { dX = h->stage + off; dldx = n; off += (size_t)n * k; }
-    ensure_buf(&h->vbuf, &h->vbuf_doubles, (size_t)n * n);
-    Ctx c = make_ctx(h, m, n, k, opts->block);
-    factor_impl(c, m, n, dA, dlda, h->vbuf, n, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts);
+    const int64_t b = opts->block;
+    const bool explicit_v = (opts->flags & UTV_EXPLICIT_V) != 0;
+    FactoredV fv;
+    if (explicit_v) {
+      ensure_buf(&h->vbuf, &h->vbuf_doubles, (size_t)n * n);
+    } else {
+      const int64_t nsteps = (n + b - 1) / b;
+      const size_t wdbl = factored_w_doubles(n, b), tdbl = (size_t)nsteps * b * b;
+      ensure_buf(&h->vbuf, &h->vbuf_doubles, wdbl + 2 * tdbl + 64);
+      fv.W = h->vbuf; fv.T = h->vbuf + wdbl; fv.Vs = fv.T + tdbl;
+    }
+    Ctx c = make_ctx(h, m, n, k, b);
+    if (explicit_v)
+      factor_impl(c, m, n, dA, dlda, h->vbuf, n, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts);
+    else
+      factor_impl(c, m, n, dA, dlda, nullptr, 0, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts, &fv);
     int64_t r = finish_factor(c, n, dA, dlda, opts->tau, true);
-    if (k > 0) solve_impl(c, n, r, dA, dlda, h->vbuf, n, dB, dldb, k, dX, dldx);
+    if (k > 0) {
+      if (explicit_v) solve_impl(c, n, r, dA, dlda, h->vbuf, n, dB, dldb, k, dX, dldx);
+      else solve_factored(c, n, r, dA, dlda, dB, dldb, k, dX, dldx, fv, b);
+    }
     // host A / B are inputs only: they are not written back (see utv.h)
     if (hX) copy2d(st, X, ldx, dX, n, n, k, cudaMemcpyDeviceToHost);
     if (hX) UTV_CUDA(cudaStreamSynchronize(st));

@@ -286,3 +286,16 @@ def test_error_statuses(utv, h):
     with pytest.raises(utv.UtvError) as e:
         utv.lstsq(dev(A), dev(np.ones((50, 1))), utv.Opts(block=16))
     assert e.value.status == utv.UTV_ERR_NUMERICAL
+
+
+@pytest.mark.parametrize("m,n,r,b,q", [(600, 520, 261, 128, 2), (300, 300, 300, 64, 1), (257, 200, 90, 32, 0)])
+def test_factored_v_equals_explicit_v(utv, m, n, r, b, q):
+    """SURVEY 8(f) #4: V = Q_1..Q_s blockdiag(V_s) applied in factored form gives the same x."""
+    M = gen.GpMatrix(m, n, r, seed=31 + m)
+    B, _ = M.known_rhs(k=2, consistent=m < 2 * r)
+    Xf, rf = _lstsq_gpu(utv, M.A, B, b, q, seed=4)
+    Ad, Bd = dev(M.A), dev(B)
+    Xe, re = utv.lstsq(Ad, Bd, utv.Opts(block=b, power_iters=q, tau=1e-10, seed=4, flags=utv.UTV_EXPLICIT_V))
+    Xe = host(Xe)
+    assert rf == re
+    assert np.linalg.norm(Xf - Xe) <= 1e-12 * np.linalg.norm(Xe)
