@@ -33,26 +33,67 @@ __host__ __device__ __forceinline__ size_t cm(int64_t i, int64_t j, int64_t ld) 
   return (size_t)i + (size_t)j * (size_t)ld;
 }
 
-// Deterministic grid barrier for cooperative launches (all CTAs co-resident).
-// bar[0] = arrival counter, bar[1] = generation.  Every CTA must call it the
-// same number of times.
+// Grid barrier for cooperative launches (all CTAs co-resident).  bar[0] = release generation
+// (written by CTA 0 only), bar[32 + c] = arrival flag of CTA c (written by CTA c only): no
+// contended atomics -- each CTA publishes its arrival with a release store, CTA 0 polls the
+// flags in parallel (one thread per CTA) and publishes the release; everyone else polls bar[0].
+// `gen` must start as bar[0] read at kernel entry; every CTA calls it the same number of times.
+// Requires >= (32 + gridDim.x) unsigned of zero-initialised (or monotone) storage.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks, unsigned& gen) {
+  const unsigned next = gen + 1;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned arrived = atomicAdd(&bar[0], 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(&bar[0], 0u);
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      volatile unsigned* vgen = bar + 1;
-      while (*vgen == gen) { __nanosleep(32); }
-    }
-    __threadfence();
+    st_release_gpu(bar + 32 + blockIdx.x, next);
   }
-  ++gen;
+  if (blockIdx.x == 0) {
+    for (unsigned c = threadIdx.x; c < nblocks; c += blockDim.x)
+      while ((int)(ld_acquire_gpu(bar + 32 + c) - next) < 0) { }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(bar, next);
+  } else if (threadIdx.x == 0) {
+    while ((int)(ld_acquire_gpu(bar) - next) < 0) { }
+  }
+  gen = next;
   __syncthreads();
 }
+
+// Single-hop variant: no master -- every CTA polls all arrival flags (one thread per CTA), so
+// the release costs one L2 round trip after the last arrival instead of two.  Same storage and
+// monotone generations as grid_sync; the caller stores the final generation to bar[0] at the end
+// of the kernel (grid_sync_finish) so the next launch starts from it.
+__device__ __forceinline__ void grid_sync_all(unsigned* bar, unsigned nblocks, unsigned& gen) {
+  const unsigned next = gen + 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu(bar + 32 + blockIdx.x, next);
+  }
+  // poll with relaxed loads (an acquire load invalidates L1 on every iteration), then one fence
+  for (unsigned c = threadIdx.x; c < nblocks; c += blockDim.x)
+    while ((int)(ld_relaxed_gpu(bar + 32 + c) - next) < 0) { }
+  __threadfence();
+  gen = next;
+  __syncthreads();
+}
+__device__ __forceinline__ void grid_sync_finish(unsigned* bar, unsigned gen) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) st_release_gpu(bar, gen);
+}
+
+constexpr size_t kGridBarrierBytes = 4096;    // >= (32 + max CTAs) * 4
 
 }  // namespace utv

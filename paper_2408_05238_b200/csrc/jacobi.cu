@@ -40,7 +40,7 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
   __shared__ unsigned s_gen;
   const int P = gridDim.x, nblk = 2 * P, c = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_gen = *((volatile unsigned*)bar + 1);
+  if (tid == 0) s_gen = ld_acquire_gpu(bar);
   __syncthreads();
   unsigned gen = s_gen;
   const double eps = 0x1.0p-52;

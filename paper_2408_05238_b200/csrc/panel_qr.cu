@@ -15,9 +15,13 @@
 //    the Gram matrix W^T W:  T_12 = -T_11 (W_1^T W_2) T_22.
 #include "kernels.cuh"
 #include "prof.cuh"
+#include <cstdlib>
 
 namespace utv {
 
+__device__ long long g_qr_trace[64 * 8];   // diagnostics: per column phase timestamps (CTA 0)
+__device__ long long g_qr_arrive[2 * 256];  // diagnostics: globaltimer at barrier arrival / departure, column 5
+__device__ __forceinline__ long long gtimer() { long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
 namespace {
 constexpr int NBMAX = 32;
 constexpr int QR_THREADS = 256;
@@ -52,7 +56,8 @@ __device__ __forceinline__ double warp_transpose_reduce(double (&a)[NBMAX]) {
 
 // Block-reduce acc[0..nb) (rows i > j of this CTA) and store this CTA's partials.
 template <bool GLOBAL>
-__device__ __forceinline__ void block_reduce_store(double (&acc)[NBMAX], int nb, double* red_w, double* part_out) {
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NBMAX], int nb, double* red_w, double* part_out,
+                                                   int stride) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double s = warp_transpose_reduce(acc);
   red_w[warp * NBMAX + lane] = s;
@@ -60,7 +65,7 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NBMAX], int nb,
   if (threadIdx.x < nb) {
     double t = 0.0;
     for (int w = 0; w < QR_THREADS / 32; ++w) t += red_w[w * NBMAX + threadIdx.x];
-    if constexpr (GLOBAL) __stcg(part_out + threadIdx.x, t);
+    if constexpr (GLOBAL) __stcg(part_out + (size_t)threadIdx.x * stride, t);
     else part_out[threadIdx.x] = t;
   }
 }
@@ -90,7 +95,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   const int64_t L = (R + G - 1) / G;
   const int64_t r0 = (int64_t)blockIdx.x * L;
   const int64_t r1 = min(R, r0 + L);
-  if (tid == 0) s_gen = *((volatile unsigned*)bar + 1);
+  if (tid == 0) s_gen = ld_acquire_gpu(bar);
   if (blockIdx.x == 0) {
     for (int64_t e = tid; e < wtop * nb; e += QR_THREADS) {   // rows above the sub-panel in W
       const int64_t i = e % wtop, c = e / wtop;
@@ -122,19 +127,37 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   // for the CTA owning pivot row j, that row at [NBMAX, NBMAX + nb).  A CTA runs at most one column
   // ahead of the slowest, so writes for column j+1 never touch the buffer read for column j, and
   // the owner updates row j in place while the others use the published copy.
-  auto slot = [&](int buf, unsigned c) { return part + ((size_t)buf * G + c) * (2 * NBMAX); };
+  // value-major: element (buf, v, c) at part[(buf * 2 NBMAX + v) * G + c], so the 32 lanes of a warp
+  // reading CTAs c..c+31 of one value touch one 256-byte segment (coalesced)
+  auto pelem = [&](int buf, int v, unsigned c) { return part + ((size_t)buf * 2 * NBMAX + v) * G + c; };
+  auto tr = [&](int j, int ph) {            // phase timestamps (build with -DUTV_QR_TRACE)
+#ifdef UTV_QR_TRACE
+    if (blockIdx.x == 0 && tid == 0 && j < 64) g_qr_trace[j * 8 + ph] = clock64();
+#else
+    (void)j; (void)ph;
+#endif
+  };
   for (int j = 0; j < nb; ++j) {
+    tr(j, 0);
     const int buf = j & 1;
     const unsigned owner = (unsigned)(j / L);
     if (G == 1) {
-      block_reduce_store<false>(acc, nb, red_w, red);
+      block_reduce_store<false>(acc, nb, red_w, red, 1);
       if (tid < nb) piv[tid] = SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)];
       __syncthreads();
     } else {
-      block_reduce_store<true>(acc, nb, red_w, slot(buf, blockIdx.x));
+      block_reduce_store<true>(acc, nb, red_w, pelem(buf, 0, blockIdx.x), (int)G);
       if (blockIdx.x == owner && tid < nb)
-        __stcg(slot(buf, owner) + NBMAX + tid, SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)]);
-      grid_sync(bar, G, gen);
+        __stcg(pelem(buf, NBMAX + tid, owner), SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)]);
+      tr(j, 3);
+#ifdef UTV_QR_TRACE
+      if (j == 5 && tid == 0 && blockIdx.x < 256) g_qr_arrive[blockIdx.x] = gtimer();
+#endif
+      grid_sync_all(bar, G, gen);
+#ifdef UTV_QR_TRACE
+      if (j == 5 && tid == 0 && blockIdx.x < 256) g_qr_arrive[256 + blockIdx.x] = gtimer();
+#endif
+      tr(j, 4);
       // fixed-order reduction of the G partials (identical in every CTA): warp w owns values
       // v = w + 8u; lane l sums CTAs c = l + 32q with all loads in flight, then a fixed butterfly
       const int warp = tid >> 5, lane = tid & 31;
@@ -146,7 +169,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
         for (int q = 0; q < QMAX; ++q) {
           const unsigned c = lane + 32u * q;
           const int v = warp + 8 * u;
-          vals[u][q] = (c < G && v < nb) ? __ldcg(slot(buf, c) + v) : 0.0;
+          vals[u][q] = (c < G && v < nb) ? __ldcg(pelem(buf, v, c)) : 0.0;
         }
 #pragma unroll
       for (int u = 0; u < NBMAX / 8; ++u) {
@@ -156,9 +179,10 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
         s = warp_sum(s);
         if (lane == 0 && warp + 8 * u < nb) red[warp + 8 * u] = s;
       }
-      if (tid < nb) piv[tid] = __ldcg(slot(buf, owner) + NBMAX + tid);
+      if (tid < nb) piv[tid] = __ldcg(pelem(buf, NBMAX + tid, owner));
       __syncthreads();
     }
+    tr(j, 1);
     if (tid == 0) {                          // dlarfg on x = P[j:, j]
       const double alpha = piv[j];
       const double xi = sqrt(red[j]);
@@ -190,20 +214,22 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     }
 #pragma unroll
     for (int v = 0; v < NBMAX; ++v) acc[v] = 0.0;
+    tr(j, 2);
     const bool next = (j + 1 < nb);
     for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
       if (i < j) continue;                   // rows above the pivot: untouched
-      // stream the row once (registers: acc only); j is runtime, so every index is static and
-      // selected with unrolled compares
-      auto ld = [&](int c) { return SMEM ? sp[(i - r0) * SROW + c] : P[cm(i, c, ldp)]; };
-      auto st = [&](int c, double x) {
-        if (SMEM) sp[(i - r0) * SROW + c] = x; else P[cm(i, c, ldp)] = x;
-      };
+      // load the whole row first (all loads in flight; no shared-memory store in between that the
+      // compiler would have to order them against), then compute, store and accumulate.  j is
+      // runtime, so every index is static and selected with unrolled compares.
+      double row[NBMAX];
+#pragma unroll
+      for (int c = 0; c < NBMAX; ++c)
+        row[c] = (c < nb) ? (SMEM ? sp[(i - r0) * SROW + c] : P[cm(i, c, ldp)]) : 0.0;
       double xj = 0.0, xj1 = 0.0, swj1 = 0.0;
 #pragma unroll
       for (int c = 0; c < NBMAX; ++c) {
-        if (c == j) xj = ld(c);
-        if (c == j + 1 && c < nb) { xj1 = ld(c); swj1 = sw[c]; }
+        if (c == j) xj = row[c];
+        if (c == j + 1) { xj1 = row[c]; swj1 = (c < nb) ? sw[c] : 0.0; }
       }
       const double v = (i == j) ? 1.0 : xj * scal;
       const double newj = (i == j) ? beta : v;   // v stored below the diagonal (LAPACK)
@@ -212,14 +238,18 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       const double xn = xj1 - tv * swj1;
 #pragma unroll
       for (int c = 0; c < NBMAX; ++c) {
-        if (c < nb) {
-          double val;
-          if (c == j) val = newj;
-          else if (c > j) val = ld(c) - tv * sw[c];
-          else val = acc_next ? ld(c) : 0.0;
-          if (c >= j) st(c, val);
-          if (acc_next) acc[c] += xn * val;
+        if (c == j) row[c] = newj;
+        else if (c > j && c < nb) row[c] -= tv * sw[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NBMAX; ++c)
+        if (c >= j && c < nb) {
+          if (SMEM) sp[(i - r0) * SROW + c] = row[c];
+          else P[cm(i, c, ldp)] = row[c];
         }
+      if (acc_next) {
+#pragma unroll
+        for (int c = 0; c < NBMAX; ++c) acc[c] += xn * row[c];
       }
     }
     __syncthreads();
@@ -237,6 +267,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       T[cm(r, c, ldt)] = sT[r * NBMAX + c];
     }
   }
+  if (G > 1) grid_sync_finish(bar, gen);
 }
 
 }  // namespace
@@ -249,8 +280,10 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
     const int nb = (int)std::min<int64_t>(NBMAX, w - jb);
     const int64_t R = rows - jb;
     // one CTA (no grid barrier) up to 1024 rows; else ~256+ rows per CTA, at most one per SM
-    const int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(std::min(pw.num_sms, 160),
-                                                                            (R + 255) / 256));
+    static const int env_max = [] { const char* e = std::getenv("UTV_QR_MAXCTAS"); return e ? std::atoi(e) : 0; }();
+    const int gmax = env_max > 0 ? std::min(env_max, pw.num_sms) : std::min(pw.num_sms, 160);
+    int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (R + 255) / 256));
+    if ((R + G - 1) / G > SMEM_ROWS_MAX && env_max > 0) G = (int)std::min<int64_t>(pw.num_sms, (R + SMEM_ROWS_MAX - 1) / SMEM_ROWS_MAX);
     const int64_t Lr = (R + G - 1) / G;
     const bool smem = Lr <= SMEM_ROWS_MAX;
     int64_t Rv = R; int nbv = nb; double* Pb = P + cm(jb, jb, ldp); double* Wb = W + cm(jb, jb, ldw);
@@ -296,3 +329,8 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
 }
 
 }  // namespace utv
+
+extern "C" int utv_debug_qr_trace(long long* out) {   // diagnostics only (not part of utv.h)
+  int e = (int)cudaMemcpyFromSymbol(out, utv::g_qr_trace, sizeof(long long) * 64 * 8);
+  return e ? e : (int)cudaMemcpyFromSymbol(out + 512, utv::g_qr_arrive, sizeof(long long) * 512);
+}

@@ -454,10 +454,10 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
     int coop = 0;
     UTV_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
     if (!coop) fail(UTV_ERR_UNSUPPORTED, "device does not support cooperative launch");
-    UTV_CUDA(cudaMalloc((void**)&h->bar, 64));
-    UTV_CUDA(cudaMemset(h->bar, 0, 64));
-    UTV_CUDA(cudaMalloc((void**)&h->bar2, 64));
-    UTV_CUDA(cudaMemset(h->bar2, 0, 64));
+    UTV_CUDA(cudaMalloc((void**)&h->bar, kGridBarrierBytes));
+    UTV_CUDA(cudaMemset(h->bar, 0, kGridBarrierBytes));
+    UTV_CUDA(cudaMalloc((void**)&h->bar2, kGridBarrierBytes));
+    UTV_CUDA(cudaMemset(h->bar2, 0, kGridBarrierBytes));
     int lo = 0, hi = 0;
     UTV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     UTV_CUDA(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
