@@ -1,13 +1,13 @@
 // gemm.cu -- FP64 tensor-core (DMMA) GEMM for sm_100a: C = alpha * op(A) op(B) + beta * C.
 //
-// This single kernel carries ~99% of randUTV's flops (SURVEY 8(a) a2, a4, a6 and the a7
+// This single kernel carries ~97% of randUTV's executed flops (SURVEY 8(a) a2, a4, a6 and the a7
 // slab updates).  B200 has no FP64 kind of tcgen05.mma, so the FP64 tensor
 // path is the warp-level `mma.sync.aligned.m16n8k4.row.col.f64` (SASS DMMA.8x8x4),
 // measured at 37.2 TFLOP/s per GPU (profiles/r01_fp64_peaks.json).
 //
 // Design (B200-first):
-//  * 128x128x16 CTA tile, 8 warps as 2 (M) x 4 (N), warp tile 64x32 = 4x4 m16n8 fragments,
-//    64 FP64 accumulators per thread; 1 CTA / SM (register bound).
+//  * CTA tile BM x BN x 16 (Shape<> table: 128x128 / 1 CTA per SM for long K, 128x64 / 2 per SM
+//    for short K), warp tile (16 MI) x (8 NJ) m16n8 fragments, 64 FP64 accumulators per thread.
 //  * Operands staged global->shared with 128-bit `cp.async.cg` (zero-fill for ragged edges)
 //    in a 4-stage ring; the layout in shared memory follows the operand's contiguous
 //    dimension (no transpose in flight): MN-major [BK][BMN+8], K-major [BMN][BK+4]; both
@@ -23,7 +23,7 @@ namespace utv {
 
 namespace {
 
-constexpr int BM = 128, BK = 16;
+constexpr int BK = 16;
 constexpr int LD_K = BK + 4;           // K-major tile row: [BMN][BK + 4]
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -53,23 +53,30 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
 template <int BMN, bool MN_MAJOR>
 constexpr int tile_doubles() { return MN_MAJOR ? BK * (BMN + 8) : BMN * LD_K; }
 
-// Tile configurations (CTA tile M is always 128; warp tile (16 MI) x 32):
-//   0: 2 x 4 warps, MI = 4 -> 128 x 128, 256 threads, 1 CTA / SM (64 accumulators / thread)
-//   1: 2 x 2 warps, MI = 4 -> 128 x  64, 128 threads, 2 CTAs / SM (short K: one CTA's epilogue
+// Tile configurations: CTA tile BM x BN, WM x WN warps, warp tile (16 MI) x (8 NJ), MI*NJ*4 = 64
+// FP64 accumulators per thread.
+//   0: 128 x 128, 2 x 4 warps of 64 x 32, 256 threads, 1 CTA / SM   (long K)
+//   1: 128 x  64, 2 x 2 warps of 64 x 32, 128 threads, 2 CTAs / SM  (short K: one CTA's epilogue
 //      overlaps the other's main loop)
-//   2: 4 x 4 warps, MI = 2 -> 128 x 128, 512 threads, 1 CTA / SM (16 warps: more latency hiding)
-//   3: 4 x 2 warps, MI = 2 -> 128 x  64, 256 threads, 2 CTAs / SM
+//   2: 128 x 128, 4 x 2 warps of 32 x 64, 256 threads, 1 CTA / SM
+//   3:  64 x 128, 2 x 2 warps of 32 x 64, 128 threads, 2 CTAs / SM
 template <int ID> struct Shape;
-template <> struct Shape<0> { static constexpr int WM = 2, WN = 4, MI = 4, CTAS = 1; };
-template <> struct Shape<1> { static constexpr int WM = 2, WN = 2, MI = 4, CTAS = 2; };
-template <> struct Shape<2> { static constexpr int WM = 4, WN = 4, MI = 2, CTAS = 1; };
-template <> struct Shape<3> { static constexpr int WM = 4, WN = 2, MI = 2, CTAS = 2; };
+template <> struct Shape<0> { static constexpr int BM = 128, WM = 2, WN = 4, MI = 4, NJ = 4, CTAS = 1; };
+template <> struct Shape<1> { static constexpr int BM = 128, WM = 2, WN = 2, MI = 4, NJ = 4, CTAS = 2; };
+template <> struct Shape<2> { static constexpr int BM = 128, WM = 4, WN = 2, MI = 2, NJ = 8, CTAS = 1; };
+template <> struct Shape<3> { static constexpr int BM = 64, WM = 2, WN = 2, MI = 2, NJ = 8, CTAS = 2; };
+constexpr int kNumShapes = 4;
+__host__ __device__ constexpr int shape_bm(int id) { return id == 3 ? 64 : 128; }
+__host__ __device__ constexpr int shape_bn(int id) { return id == 1 ? 64 : 128; }
+__host__ __device__ constexpr int shape_ctas(int id) { return (id == 1 || id == 3) ? 2 : 1; }
 
 template <bool TA, bool TB, int ID>
 struct Cfg {
-  static constexpr int WM = Shape<ID>::WM, WN = Shape<ID>::WN, MI = Shape<ID>::MI;
-  static_assert(16 * MI * WM == BM, "CTA tile M must be 128");
-  static constexpr int BN = 32 * WN;
+  static constexpr int BM = Shape<ID>::BM, WM = Shape<ID>::WM, WN = Shape<ID>::WN;
+  static constexpr int MI = Shape<ID>::MI, NJ = Shape<ID>::NJ;
+  static_assert(16 * MI * WM == BM, "warp tiles must cover BM");
+  static constexpr int BN = 8 * NJ * WN;
+  static_assert(BM == shape_bm(ID) && BN == shape_bn(ID), "shape table out of sync");
   static constexpr int THREADS = 32 * WM * WN;
   static constexpr bool A_MN = !TA, B_MN = TB;
   static constexpr int A_DBL = tile_doubles<BM, A_MN>();
@@ -127,8 +134,8 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
                   const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
                   int64_t k_chunk, double* __restrict__ partial) {
   using CF = Cfg<TA, TB, ID>;
-  constexpr int BN = CF::BN, THREADS = CF::THREADS, STAGES = CF::STAGES;
-  constexpr int WN = CF::WN, MI = CF::MI, WTM = 16 * MI;   // warp tile WTM x 32
+  constexpr int BM = CF::BM, BN = CF::BN, THREADS = CF::THREADS, STAGES = CF::STAGES;
+  constexpr int WN = CF::WN, MI = CF::MI, NJ = CF::NJ, WTM = 16 * MI, WTN = 8 * NJ;
   constexpr bool A_MN = CF::A_MN, B_MN = CF::B_MN;
   extern __shared__ __align__(128) double smem[];
 
@@ -151,11 +158,11 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
   const int wm = warp / WN, wn = warp % WN;      // WM x WN warps
   const int g = lane >> 2, t = lane & 3;
 
-  double acc[MI][4][4];
+  double acc[MI][NJ][4];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
 
@@ -175,7 +182,7 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
   // Software pipeline: the fragments of k-step s+1 are loaded (LDS) while the DMMAs of step s
   // run (register double buffer), and the barrier that publishes the next stage is taken
   // before the last k-step of the current one, so its latency overlaps 16 DMMAs.
-  double af[2][MI][2], bf[2][4];
+  double af[2][MI][2], bf[2][NJ];
   auto load_frags = [&](int buf, const double* sa, const double* sb, int kk) {
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
@@ -184,7 +191,7 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
       af[buf][i][1] = frag<BM, A_MN>(sa, mr + 8, kk + t);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) bf[buf][j] = frag<BN, B_MN>(sb, wn * 32 + j * 8 + g, kk + t);
+    for (int j = 0; j < NJ; ++j) bf[buf][j] = frag<BN, B_MN>(sb, wn * WTN + j * 8 + g, kk + t);
   };
 
   cp_async_wait<STAGES - 2>();
@@ -216,7 +223,7 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
+        for (int j = 0; j < NJ; ++j) dmma_16x8x4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
     }
   }
   cp_async_wait<0>();
@@ -227,11 +234,11 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
-          const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
+          const int64_t n = n0 + wn * WTN + j * 8 + 2 * t + (r & 1);
           if (m < M && n < N) P[cm(m, n, M)] = acc[i][j][r];
         }
   } else {
@@ -240,11 +247,11 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
-            const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
+            const int64_t n = n0 + wn * WTN + j * 8 + 2 * t + (r & 1);
             const double c = (m < M && n < N) ? __ldg(C + cm(m, n, ldc)) : 0.0;
             acc[i][j][r] = alpha * acc[i][j][r] + beta * c;
           }
@@ -252,244 +259,21 @@ dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* _
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] *= alpha;
     }
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
-          const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
+          const int64_t n = n0 + wn * WTN + j * 8 + 2 * t + (r & 1);
           if (m < M && n < N) C[cm(m, n, ldc)] = acc[i][j][r];
         }
   }
-}
-
-// ------------------------------------------------------------------------------------------
-// v2 main loop (default): fragments fetched with 128-bit LDS from an "interleave-by-8" shared
-// layout, operands staged with 8-byte cp.async (any alignment / leading dimension).
-//   position of mn inside a 16-row group: 2 (mn mod 8) + (mn div 8 mod 2), so the two values a
-//   thread needs for rows mn and mn + 8 (A: a0/a1 of m16n8k4; B: b0 of n8-tiles j and j+1) are
-//   adjacent -> one LDS.128 instead of two LDS.64 (6 instead of 12 loads per 16 MMAs).
-//   MN-major tile: [BK][BMN + 4] (row stride = 4 mod 16 doubles), K-major tile: [BMN/2][BK][2]
-//   with pair-row stride 40 doubles; both give conflict-free quarter-warp phases for LDS.128.
-template <int BMN, bool MN_MAJOR>
-__device__ __forceinline__ int sidx2(int mn, int k) {
-  const int hi = (mn >> 3) & 1;
-  if constexpr (MN_MAJOR) return k * (BMN + 4) + ((mn & ~15) | ((mn & 7) << 1) | hi);
-  else return (((mn & ~15) >> 1) | (mn & 7)) * 40 + k * 2 + hi;
-}
-template <int BMN, bool MN_MAJOR>
-constexpr int tile_doubles2() { return MN_MAJOR ? BK * (BMN + 4) : (BMN / 2) * 40; }
-
-template <bool TA, bool TB, int ID>
-struct Cfg2 {
-  static constexpr int WM = Shape<ID>::WM, WN = Shape<ID>::WN, MI = Shape<ID>::MI;
-  static constexpr int BN = 32 * WN;
-  static constexpr int THREADS = 32 * WM * WN;
-  static constexpr bool A_MN = !TA, B_MN = TB;
-  static constexpr int A_DBL = tile_doubles2<BM, A_MN>();
-  static constexpr int B_DBL = tile_doubles2<BN, B_MN>();
-  static constexpr int STAGE_DBL = A_DBL + B_DBL;
-  static constexpr int CTAS_PER_SM = Shape<ID>::CTAS;
-  static constexpr int SMEM_BUDGET = (CTAS_PER_SM == 1 ? 200 : 110) * 1024;
-  static constexpr int STAGES_FIT = SMEM_BUDGET / (STAGE_DBL * 8);
-  static constexpr int STAGES = STAGES_FIT > 4 ? 4 : STAGES_FIT;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_DBL * sizeof(double);
-  static_assert(STAGES >= 3, "not enough shared memory for a 3-stage pipeline");
-};
-
-__device__ __forceinline__ void cp_async8(unsigned dst, const double* src, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global.L2::128B [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
-}
-
-// BMN x 16 tile, one 8-byte element per copy, consecutive threads along the contiguous dimension.
-template <int BMN, bool MN_MAJOR, int THREADS>
-__device__ __forceinline__ void load_tile2(double* s, const double* __restrict__ g, int64_t ld, int64_t mn0,
-                                           int64_t MN, int64_t k0, int64_t kend) {
-  const int tid = threadIdx.x;
-  constexpr int NEL = BMN * BK;
-#pragma unroll
-  for (int e = tid; e < NEL; e += THREADS) {
-    int mm, kk;
-    if constexpr (MN_MAJOR) { kk = e / BMN; mm = e % BMN; }
-    else { mm = e / BK; kk = e % BK; }
-    const int64_t gk = k0 + kk, gm = mn0 + mm;
-    const bool ok = gk < kend && gm < MN;
-    const double* src = ok ? (MN_MAJOR ? g + gm + gk * ld : g + gk + gm * ld) : g;
-    cp_async8(smem_u32(s + sidx2<BMN, MN_MAJOR>(mm, kk)), src, ok ? 8 : 0);
-  }
-}
-
-template <bool TA, bool TB, int ID>
-__global__ void __launch_bounds__(Cfg2<TA, TB, ID>::THREADS, Cfg2<TA, TB, ID>::CTAS_PER_SM)
-dgemm_dmma2_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
-                   const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-                   int64_t k_chunk, double* __restrict__ partial) {
-  using CF = Cfg2<TA, TB, ID>;
-  constexpr int BN = CF::BN, THREADS = CF::THREADS, STAGES = CF::STAGES;
-  constexpr int WN = CF::WN, MI = CF::MI, WTM = 16 * MI;
-  constexpr bool A_MN = CF::A_MN, B_MN = CF::B_MN;
-  extern __shared__ __align__(128) double smem[];
-
-  const int64_t tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
-  constexpr int64_t GROUP_M = 16;
-  const int64_t pid = blockIdx.x;
-  const int64_t per_group = GROUP_M * tiles_n;
-  const int64_t first_m = (pid / per_group) * GROUP_M;
-  const int64_t gsz = min(tiles_m - first_m, GROUP_M);
-  const int64_t m0 = (first_m + (pid % per_group) % gsz) * BM;
-  const int64_t n0 = ((pid % per_group) / gsz) * BN;
-  const int64_t kbeg = (int64_t)blockIdx.z * k_chunk;
-  const int64_t kend = min(K, kbeg + k_chunk);
-  const int nkt = (int)((kend - kbeg + BK - 1) / BK);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp / WN, wn = warp % WN;
-  const int g = lane >> 2, t = lane & 3;
-
-  double acc[MI][4][4];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
-
-  auto stage_a = [&](int s) { return smem + s * CF::STAGE_DBL; };
-  auto stage_b = [&](int s) { return smem + s * CF::STAGE_DBL + CF::A_DBL; };
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nkt) {
-      const int64_t k0 = kbeg + (int64_t)s * BK;
-      load_tile2<BM, A_MN, THREADS>(stage_a(s), A, lda, m0, M, k0, kend);
-      load_tile2<BN, B_MN, THREADS>(stage_b(s), B, ldb, n0, N, k0, kend);
-    }
-    cp_async_commit();
-  }
-
-  double2 af[2][MI], bf[2][2];
-  auto load_frags = [&](int buf, const double* sa, const double* sb, int kk) {
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-      af[buf][i] = *reinterpret_cast<const double2*>(sa + sidx2<BM, A_MN>(wm * WTM + i * 16 + g, kk + t));
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-      bf[buf][u] = *reinterpret_cast<const double2*>(sb + sidx2<BN, B_MN>(wn * 32 + u * 16 + g, kk + t));
-  };
-
-  cp_async_wait<STAGES - 2>();
-  __syncthreads();
-  if (nkt > 0) load_frags(0, stage_a(0), stage_b(0), 0);
-
-  for (int kt = 0; kt < nkt; ++kt) {
-    const double* sa = stage_a(kt % STAGES);
-    const double* sb = stage_b(kt % STAGES);
-#pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-      const int cur = ks & 1;
-      if (ks == BK / 4 - 1) {
-        cp_async_wait<STAGES - 3 >= 0 ? STAGES - 3 : 0>();
-        __syncthreads();
-        const int pf = kt + STAGES - 1;
-        if (pf < nkt) {
-          const int s = pf % STAGES;
-          const int64_t k0 = kbeg + (int64_t)pf * BK;
-          load_tile2<BM, A_MN, THREADS>(stage_a(s), A, lda, m0, M, k0, kend);
-          load_tile2<BN, B_MN, THREADS>(stage_b(s), B, ldb, n0, N, k0, kend);
-        }
-        cp_async_commit();
-        if (kt + 1 < nkt) load_frags(cur ^ 1, stage_a((kt + 1) % STAGES), stage_b((kt + 1) % STAGES), 0);
-      } else {
-        load_frags(cur ^ 1, sa, sb, (ks + 1) * 4);
-      }
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double b0 = (j & 1) ? bf[cur][j >> 1].y : bf[cur][j >> 1].x;
-          dmma_16x8x4(acc[i][j], af[cur][i].x, af[cur][i].y, b0);
-        }
-    }
-  }
-  cp_async_wait<0>();
-
-  // Epilogue (fragment (i, j): rows m0+wm*WTM+i*16+g (+8), cols n0+wn*32+j*8+2t (+1)).
-  if (partial) {
-    double* P = partial + (size_t)blockIdx.z * (size_t)M * (size_t)N;
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
-          const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
-          if (m < M && n < N) P[cm(m, n, M)] = acc[i][j][r];
-        }
-  } else {
-    if (beta != 0.0) {
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
-            const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
-            const double c = (m < M && n < N) ? __ldg(C + cm(m, n, ldc)) : 0.0;
-            acc[i][j][r] = alpha * acc[i][j][r] + beta * c;
-          }
-    } else {
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) acc[i][j][r] *= alpha;
-    }
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int64_t m = m0 + wm * WTM + i * 16 + g + (r >> 1) * 8;
-          const int64_t n = n0 + wn * 32 + j * 8 + 2 * t + (r & 1);
-          if (m < M && n < N) C[cm(m, n, ldc)] = acc[i][j][r];
-        }
-  }
-}
-
-template <bool TA, bool TB, int ID>
-void launch_v2(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splits, int64_t kc,
-               double* partial) {
-  using CF = Cfg2<TA, TB, ID>;
-  static bool attr_set = false;
-  auto kern = dgemm_dmma2_kernel<TA, TB, ID>;
-  if (!attr_set) {
-    UTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
-    attr_set = true;
-  }
-  dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + BM - 1) / BM)), 1u, (unsigned)splits);
-  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial);
-  UTV_CUDA(cudaGetLastError());
-}
-
-template <int ID>
-void dispatch_v2(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
-                 int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splits,
-                 int64_t kc, double* partial) {
-  if (!ta && !tb) launch_v2<false, false, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else if (ta && !tb) launch_v2<true, false, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else if (!ta && tb) launch_v2<false, true, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
-  else launch_v2<true, true, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
 }
 
 // C = alpha * sum_{z=0}^{S-1} partial[z] + beta * C, summed in order z = 0..S-1.
@@ -517,7 +301,7 @@ void launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, co
     UTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
     attr_set = true;
   }
-  dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + BM - 1) / BM)), 1u, (unsigned)splits);
+  dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + CF::BM - 1) / CF::BM)), 1u, (unsigned)splits);
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial);
   UTV_CUDA(cudaGetLastError());
 }
@@ -547,24 +331,24 @@ int g_cfg_long = 0, g_cfg_short = 1;     // defaults (overridable: UTV_GEMM_CFG_
 
 static Plan make_plan(int64_t M, int64_t N, int64_t K, int num_sms, size_t work_doubles) {
   static const bool env_read = [] {
-    if (const char* e = std::getenv("UTV_GEMM_CFG_LONG")) g_cfg_long = std::atoi(e) & 3;
-    if (const char* e = std::getenv("UTV_GEMM_CFG_SHORT")) g_cfg_short = std::atoi(e) & 3;
+    if (const char* e = std::getenv("UTV_GEMM_CFG_LONG")) g_cfg_long = std::atoi(e) % kNumShapes;
+    if (const char* e = std::getenv("UTV_GEMM_CFG_SHORT")) g_cfg_short = std::atoi(e) % kNumShapes;
     return true;
   }();
   (void)env_read;
   const int cfg = g_force_wn ? g_force_wn : (K <= 1024 ? g_cfg_short : g_cfg_long);
-  const int bn = (cfg == 1 || cfg == 3) ? 64 : 128, ctas = (cfg == 1 || cfg == 3) ? 2 : 1;
+  const int bm = shape_bm(cfg), bn = shape_bn(cfg), ctas = shape_ctas(cfg);
   Plan best{cfg, 1, K};
   double best_t = 1e300;
   const double slots = (double)num_sms * ctas;
-  const double tiles = (double)((M + BM - 1) / BM) * (double)((N + bn - 1) / bn);
+  const double tiles = (double)((M + bm - 1) / bm) * (double)((N + bn - 1) / bn);
   const double rate = 37.2e12 * 0.85 / slots;              // flop/s per CTA slot
   for (int s = 1; s <= 128; ++s) {
     if (s > 1 && (K / s < 256 || (size_t)s * (size_t)M * (size_t)N > work_doubles)) break;
     const int64_t kc = s == 1 ? K : ((K + s - 1) / s + BK - 1) / BK * BK;
     const int sp = (int)((K + kc - 1) / kc);
     const double waves = std::ceil(tiles * sp / slots);
-    double t = waves * (2.0 * BM * bn * (double)kc / rate + 2.5e-6);
+    double t = waves * (2.0 * bm * bn * (double)kc / rate + 2.5e-6);
     if (sp > 1) t += 8.0 * (double)M * (double)N * (sp + 1) / 5.0e12 + 4e-6;
     if (t < best_t * 0.995) { best_t = t; best = Plan{cfg, sp, kc}; }
   }
@@ -601,20 +385,15 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
   ProfScope prof(st, kProfGemm, splits > 1 ? 2 : 1, 2.0 * (double)M * (double)N * (double)K,
                  8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2.0 : 1.0)));
   prof.shape(M, N, K, (ta ? 1 : 0) | (tb ? 2 : 0) | (plan.cfg << 2) | (splits << 8));
-  static const int use_v1 = [] { const char* e = std::getenv("UTV_GEMM_V1"); return e ? std::atoi(e) : 0; }();
-  if (!use_v1) {
-    switch (plan.cfg) {
-      case 0: dispatch_v2<0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-      case 1: dispatch_v2<1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-      case 2: dispatch_v2<2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-      default: dispatch_v2<3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    }
-  } else switch (plan.cfg | (aligned ? 0 : 4)) {
+  switch (plan.cfg | (aligned ? 0 : 4)) {
     case 0: dispatch<2, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
     case 1: dispatch<2, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
     case 2: dispatch<2, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
     case 3: dispatch<2, 3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    default: dispatch<1, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    case 4: dispatch<1, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    case 5: dispatch<1, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    case 6: dispatch<1, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+    default: dispatch<1, 3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
   }
   if (splits > 1) {
     const int64_t total = M * N;
