@@ -6,8 +6,8 @@
 // explicit Q, column signs flipped so R'_jj >= 0, sigma_j := R'_jj.
 //
 // B200 design: block one-sided Jacobi.  The b columns are split into 2P blocks of 16; a
-// cooperative grid of P CTAs (P = ceil(b/32), 8 at b = 256) runs a round-robin tournament over
-// the blocks (2P-1 rounds per sweep, one grid barrier per round).  In each round a CTA stages
+// thread-block cluster of P CTAs (P = ceil(b/32), 8 at b = 256) runs a round-robin tournament over
+// the blocks (2P-1 rounds per sweep, one hardware cluster barrier per round).  In each round a CTA stages
 // its two blocks (32 columns of W and of J, 128 KiB at b = 256) in shared memory and runs a
 // full inner cyclic sweep over the 496 column pairs, 16 disjoint pairs at a time (one warp per
 // pair, 8 rows per lane, fixed-order warp reductions broadcast from lane 0).  The pair order
@@ -18,9 +18,17 @@
 
 namespace utv {
 
+__device__ long long g_jac_trace[32 * 8];   // diagnostics (-DUTV_JAC_TRACE): CTA 0 phase clocks
 namespace {
 constexpr int JBLK = 16;
 constexpr int JT = 512;
+
+__device__ __forceinline__ void cluster_barrier() {
+  // hardware cluster barrier (~0.2 us): release / acquire order the global-memory column
+  // exchange between the CTAs of the cluster
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 
 __device__ __forceinline__ double warp_sum_bcast(double v) {
 #pragma unroll
@@ -36,13 +44,11 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
   double* sJ = jsm + 2 * JBLK * bw;
   __shared__ int s_gcol[2 * JBLK];
   __shared__ int s_rot;
+  __shared__ double s_nrm[2 * JBLK];
   __shared__ int s_done;
-  __shared__ unsigned s_gen;
   const int P = gridDim.x, nblk = 2 * P, c = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_gen = ld_acquire_gpu(bar);
-  __syncthreads();
-  unsigned gen = s_gen;
+  (void)bar;
   const double eps = 0x1.0p-52;
   const double small2 = eps * eps * fro2[0];   // R9b: numerically-zero column floor
 
@@ -50,23 +56,49 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
   bool converged = false;
   for (sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int r = 0; r < nblk - 1; ++r) {
+#ifdef UTV_JAC_TRACE
+      const int trk = sweep * 15 + r;
+      if (c == 0 && tid == 0 && trk < 32) g_jac_trace[trk * 8 + 0] = clock64();
+#endif
       const int bp = (c == 0) ? 0 : 1 + (c - 1 + r) % (nblk - 1);
       const int kq = nblk - 1 - c;
       const int bq = (kq == 0) ? 0 : 1 + (kq - 1 + r) % (nblk - 1);
       if (tid < 2 * JBLK) s_gcol[tid] = tid < JBLK ? bp * JBLK + tid : bq * JBLK + (tid - JBLK);
       if (tid == 0) s_rot = 0;
       __syncthreads();
-      // stage the 32 columns (all loads of a thread in flight together: <= 16 per matrix)
+      // stage the 32 columns: all global loads of a thread in flight, then the shared stores
+      constexpr int PER = 2 * JBLK * 256 / JT;
+      {
+        double lw[PER], lj[PER];
 #pragma unroll
-      for (int it = 0; it < 2 * JBLK * 256 / JT; ++it) {
-        const int e = tid + it * JT;
-        if (e < 2 * JBLK * bw) {
-          const int col = e / bw, row = e % bw, gc = s_gcol[col];
-          sW[e] = gc < bw ? __ldcg(W + (size_t)gc * bw + row) : 0.0;
-          sJ[e] = gc < bw ? __ldcg(J + (size_t)gc * bw + row) : 0.0;
+        for (int it = 0; it < PER; ++it) {
+          const int e = tid + it * JT;
+          const bool valid = e < 2 * JBLK * bw;
+          const int col = valid ? e / bw : 0, row = valid ? e % bw : 0, gc = s_gcol[col];
+          const bool ok = valid && gc < bw;
+          lw[it] = ok ? __ldcg(W + (size_t)gc * bw + row) : 0.0;
+          lj[it] = ok ? __ldcg(J + (size_t)gc * bw + row) : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < PER; ++it) {
+          const int e = tid + it * JT;
+          if (e < 2 * JBLK * bw) { sW[e] = lw[it]; sJ[e] = lj[it]; }
         }
       }
       __syncthreads();
+      // squared column norms, recomputed from the data once per round and then updated exactly
+      // per rotation (alpha' = alpha - t gamma, beta' = beta + t gamma): one inner product per pair
+      for (int col = warp; col < 2 * JBLK; col += JT / 32) {
+        double s2 = 0.0;
+        for (int row = lane; row < bw; row += 32) s2 += sW[col * bw + row] * sW[col * bw + row];
+        s2 = warp_sum_bcast(s2);
+        if (lane == 0) s_nrm[col] = s2;
+      }
+      __syncthreads();
+#ifdef UTV_JAC_TRACE
+      if (c == 0 && tid == 0 && trk < 32) g_jac_trace[trk * 8 + 1] = clock64();
+#endif
+      constexpr int RPL = 256 / 32;                    // rows per lane (bw <= 256)
       for (int ir = 0; ir < 2 * JBLK - 1; ++ir) {
         if (warp < JBLK) {
           int a = (warp == 0) ? 0 : 1 + (warp - 1 + ir) % (2 * JBLK - 1);
@@ -77,47 +109,86 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
           if (gb < bw) {
             double* wi = sW + a * bw;
             double* wj = sW + b * bw;
-            double al = 0.0, be = 0.0, gm = 0.0;
-            for (int row = lane; row < bw; row += 32) {
-              const double x = wi[row], y = wj[row];
-              al += x * x; be += y * y; gm += x * y;
+            double x[RPL], y[RPL];
+#pragma unroll
+            for (int k = 0; k < RPL; ++k) {
+              const int row = lane + 32 * k;
+              x[k] = row < bw ? wi[row] : 0.0;
+              y[k] = row < bw ? wj[row] : 0.0;
             }
-            al = warp_sum_bcast(al); be = warp_sum_bcast(be); gm = warp_sum_bcast(gm);
-            const bool skip = (gm == 0.0) || al <= small2 || be <= small2 || fabs(gm) <= tol * sqrt(al) * sqrt(be);
+            double gm = 0.0;
+#pragma unroll
+            for (int k = 0; k < RPL; ++k) gm += x[k] * y[k];
+            gm = warp_sum_bcast(gm);
+            const double al = s_nrm[a], be = s_nrm[b];
+            const bool skip = (gm == 0.0) || al <= small2 || be <= small2 || fabs(gm) <= tol * sqrt(al * be);
             if (!skip) {
-              const double zeta = (be - al) / (2.0 * gm);
-              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              const double cs = 1.0 / sqrt(1.0 + t * t);
+              // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 gm), rewritten
+              // as t = 2 gm sign(be - al) / (|be - al| + sqrt((be - al)^2 + 4 gm^2)) (one division)
+              const double d = be - al;
+              const double t = (d >= 0.0 ? 2.0 * gm : -2.0 * gm) / (fabs(d) + sqrt(d * d + 4.0 * gm * gm));
+              const double cs = rsqrt(1.0 + t * t);
               const double sn = cs * t;
               double* ji = sJ + a * bw;
               double* jj = sJ + b * bw;
-              for (int row = lane; row < bw; row += 32) {
-                const double x = wi[row], y = wj[row];
-                wi[row] = cs * x - sn * y;
-                wj[row] = sn * x + cs * y;
-                const double u = ji[row], v = jj[row];
-                ji[row] = cs * u - sn * v;
-                jj[row] = sn * u + cs * v;
+              double u[RPL], v[RPL];
+#pragma unroll
+              for (int k = 0; k < RPL; ++k) {
+                const int row = lane + 32 * k;
+                u[k] = row < bw ? ji[row] : 0.0;
+                v[k] = row < bw ? jj[row] : 0.0;
               }
-              if (lane == 0) atomicAdd(&s_rot, 1);
+#pragma unroll
+              for (int k = 0; k < RPL; ++k) {
+                const int row = lane + 32 * k;
+                if (row < bw) {
+                  wi[row] = cs * x[k] - sn * y[k];
+                  wj[row] = sn * x[k] + cs * y[k];
+                  ji[row] = cs * u[k] - sn * v[k];
+                  jj[row] = sn * u[k] + cs * v[k];
+                }
+              }
+              if (lane == 0) {
+                s_nrm[a] = fmax(al - t * gm, 0.0);
+                s_nrm[b] = be + t * gm;
+                atomicAdd(&s_rot, 1);
+              }
             }
           }
         }
         __syncthreads();
       }
+#ifdef UTV_JAC_TRACE
+      if (c == 0 && tid == 0 && trk < 32) g_jac_trace[trk * 8 + 2] = clock64();
+#endif
+      {
+        double lw[PER], lj[PER];
 #pragma unroll
-      for (int it = 0; it < 2 * JBLK * 256 / JT; ++it) {
-        const int e = tid + it * JT;
-        if (e < 2 * JBLK * bw) {
-          const int col = e / bw, row = e % bw, gc = s_gcol[col];
-          if (gc < bw) {
-            __stcg(W + (size_t)gc * bw + row, sW[e]);
-            __stcg(J + (size_t)gc * bw + row, sJ[e]);
+        for (int it = 0; it < PER; ++it) {
+          const int e = tid + it * JT;
+          lw[it] = e < 2 * JBLK * bw ? sW[e] : 0.0;
+          lj[it] = e < 2 * JBLK * bw ? sJ[e] : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < PER; ++it) {
+          const int e = tid + it * JT;
+          if (e < 2 * JBLK * bw) {
+            const int col = e / bw, row = e % bw, gc = s_gcol[col];
+            if (gc < bw) {
+              __stcg(W + (size_t)gc * bw + row, lw[it]);
+              __stcg(J + (size_t)gc * bw + row, lj[it]);
+            }
           }
         }
       }
+#ifdef UTV_JAC_TRACE
+      if (c == 0 && tid == 0 && trk < 32) g_jac_trace[trk * 8 + 3] = clock64();
+#endif
       if (tid == 0 && s_rot) atomicAdd(rot + sweep, s_rot);
-      grid_sync(bar, P, gen);
+      cluster_barrier();
+#ifdef UTV_JAC_TRACE
+      if (c == 0 && tid == 0 && trk < 32) g_jac_trace[trk * 8 + 4] = clock64();
+#endif
     }
     if (tid == 0) s_done = (atomicAdd(rot + sweep, 0) == 0);
     __syncthreads();
@@ -216,7 +287,22 @@ void svd_small(cudaStream_t st, int64_t bw64, const double* R, int64_t ldr, doub
   int maxs = kMaxSweeps;
   void* args[] = {&bwv, (void*)&sw.W, (void*)&sw.J, &fro2, &tol, &maxs, (void*)&sw.rot, (void*)&sw.info,
                   (void*)&sw.pw.bar};
-  UTV_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_kernel, dim3(P), dim3(JT), args, smem, st));
+  {
+    // one thread-block cluster of P <= 8 CTAs (portable size): cluster barriers between rounds
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(JT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    UTV_CUDA(cudaLaunchKernelExC(&cfg, (const void*)jacobi_kernel, args));
+  }
   jacobi_sort_kernel<<<1, 256, 0, st>>>(bw, sw.W, sw.J, sw.Ws, Us, ldu);
   UTV_CUDA(cudaGetLastError());
   }
@@ -231,3 +317,7 @@ void svd_small(cudaStream_t st, int64_t bw64, const double* R, int64_t ldr, doub
 }
 
 }  // namespace utv
+
+extern "C" int utv_debug_jac_trace(long long* out) {   // diagnostics only (not part of utv.h)
+  return (int)cudaMemcpyFromSymbol(out, utv::g_jac_trace, sizeof(long long) * 32 * 8);
+}
