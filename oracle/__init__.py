@@ -53,6 +53,9 @@ def lib():
         _lib.oracle_solve.argtypes = [i64, i64, d, i64, d, i64, d, i64, i64, d, i64]
         _lib.oracle_lstsq.argtypes = [i64, i64, i64, d, i64, d, i64, d, i64, i64, i32, C.c_double, u64, d]
         _lib.oracle_lstsq.restype = C.c_int
+        _lib.oracle_nullify.argtypes = [i64, i64, d, i64, d, i64]
+        _lib.oracle_lstsq_ex.argtypes = [i64, i64, i64, d, i64, d, i64, d, i64, i64, i32, C.c_double, u64, C.c_int, d]
+        _lib.oracle_lstsq_ex.restype = C.c_int
         _lib.oracle_set_threads.argtypes = [C.c_int]
         _lib.oracle_get_threads.restype = C.c_int
     return _lib
@@ -146,14 +149,21 @@ def solve(T, V, Cm, r: int):
     return X
 
 
-def lstsq(A, B, b: int, q: int, tau: float = 1e-10, seed: int = 1):
-    """Fast-option randUTV least squares (fig:alg_axb without Nullify). Returns (X, r)."""
+def nullify(T, V, r: int):
+    """Nullify_top_right_part_of_T (fig:alg_nullify_t12): returns (T', V') with T'(0:r, r:n) = 0."""
+    T = _f64(T); V = _f64(V); n = V.shape[0]
+    lib().oracle_nullify(n, int(r), _p(T), max(T.shape[0], 1), _p(V), max(n, 1))
+    return T, V
+
+
+def lstsq(A, B, b: int, q: int, tau: float = 1e-10, seed: int = 1, nullify: bool = False):
+    """randUTV least squares (fig:alg_axb; fast option without Nullify unless nullify=True). Returns (X, r)."""
     A = _f64(A); m, n = A.shape
     B2 = _f64(np.asarray(B).reshape(m, -1)); k = B2.shape[1]
     X = np.zeros((n, k), order="F")
     r = C.c_int64(0)
-    st = lib().oracle_lstsq(m, n, k, _p(A), max(m, 1), _p(B2), max(m, 1), _p(X), max(n, 1), b, q, float(tau),
-                            seed, C.byref(r))
+    st = lib().oracle_lstsq_ex(m, n, k, _p(A), max(m, 1), _p(B2), max(m, 1), _p(X), max(n, 1), b, q, float(tau),
+                               seed, int(bool(nullify)), C.byref(r))
     if st != OK:
         raise OracleError(st)
     return X, int(r.value)

@@ -25,6 +25,8 @@
  *                             RSVD identity P:848-858)
  *   rank / solve / lstsq ... pinned (pinv brute force on exact-rank inputs,
  *                             numpy.linalg.solve for full rank, known solution)
+ *   nullify ................ pinned (T12 == 0, V orthogonal, A = U T V^T kept, and
+ *                             x = pinv(U_1 [T11 T12] V^T) b by brute force)
  */
 #include <math.h>
 #include <stdint.h>
@@ -521,11 +523,59 @@ void oracle_solve(int64_t n, int64_t r, const double* T, int64_t ldt, const doub
 }
 
 /* ------------------------------------------------------------------------- */
+/* Nullify_top_right_part_of_T (fig:alg_nullify_t12; "conforming to */
+/* the xGELSY functions" P:902-907): an RZ sweep from the right that zeroes    */
+/* T12 = T(0:r, r:n) and updates V.  Row by row from the bottom (the blocked    */
+/* Nullify / Update of the figure, one row per block): for i = r-1 .. 0,       */
+/* dlarfg on x = [T(i,i), T(i, r:n)] gives beta, tau, v = [1; z]; the           */
+/* reflector H = I - tau v v^T acts on columns (i, r:n) of the rows above       */
+/* (Update(C11, D1, C01, D0)) and of V (Update(C11, D1, E1, F)); then           */
+/* T(i,i) = beta and T(i, r:n) = 0.  Rows below i already have zeros in T12    */
+/* and in column i, so they are unaffected.                                    */
+/* ------------------------------------------------------------------------- */
+void oracle_nullify(int64_t n, int64_t r, double* T, int64_t ldt, double* V, int64_t ldv) {
+  const int64_t nz = n - r;
+  if (nz <= 0 || r <= 0) return;
+  double* z = dalloc(nz);
+  for (int64_t i = r - 1; i >= 0; --i) {
+    const double alpha = T[IDX(i, i, ldt)];
+    double xi2 = 0.0;
+    for (int64_t l = 0; l < nz; ++l) xi2 += T[IDX(i, r + l, ldt)] * T[IDX(i, r + l, ldt)];
+    const double xi = sqrt(xi2);
+    if (xi == 0.0) continue;                       /* tau = 0: H = I */
+    const double beta = -copysign(hypot(alpha, xi), alpha);
+    const double tau = (beta - alpha) / beta;
+    const double scal = 1.0 / (alpha - beta);
+    for (int64_t l = 0; l < nz; ++l) z[l] = T[IDX(i, r + l, ldt)] * scal;
+    for (int64_t k = 0; k < i; ++k) {              /* rows above: x_k <- x_k H */
+      double w = T[IDX(k, i, ldt)];
+      for (int64_t l = 0; l < nz; ++l) w += T[IDX(k, r + l, ldt)] * z[l];
+      w *= tau;
+      T[IDX(k, i, ldt)] -= w;
+      for (int64_t l = 0; l < nz; ++l) T[IDX(k, r + l, ldt)] -= w * z[l];
+    }
+    if (V) {
+      for (int64_t k = 0; k < n; ++k) {            /* V <- V H */
+        double w = V[IDX(k, i, ldv)];
+        for (int64_t l = 0; l < nz; ++l) w += V[IDX(k, r + l, ldv)] * z[l];
+        w *= tau;
+        V[IDX(k, i, ldv)] -= w;
+        for (int64_t l = 0; l < nz; ++l) V[IDX(k, r + l, ldv)] -= w * z[l];
+      }
+    }
+    T[IDX(i, i, ldt)] = beta;
+    for (int64_t l = 0; l < nz; ++l) T[IDX(i, r + l, ldt)] = 0.0;
+  }
+  free(z);
+}
+
+/* ------------------------------------------------------------------------- */
 /* Solve_linear_system, fast option (fig:alg_axb P:1075-1108 without the       */
 /* Nullify line, "Fast option" P:1114-1121; v24s/v34s).  A and B consumed.    */
 /* ------------------------------------------------------------------------- */
-int oracle_lstsq(int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
-                 double* X, int64_t ldx, int64_t nb, int32_t q, double tau, uint64_t seed, int64_t* rank) {
+int oracle_lstsq_ex(int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
+                    double* X, int64_t ldx, int64_t nb, int32_t q, double tau, uint64_t seed, int nullify,
+                    int64_t* rank) {
   if (m < n) return ORACLE_ERR_SHAPE;
   if (!(tau >= 0.0 && tau < 1.0) || ldx < n) return ORACLE_ERR_ARG;
   double* V = dalloc(n * n);
@@ -533,8 +583,14 @@ int oracle_lstsq(int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double
   int st = oracle_randutv(m, n, k, A, lda, V, n, NULL, 0, B, ldb, nb, q, seed, NULL);
   if (st != ORACLE_OK) { free(V); return st; }
   int64_t r = oracle_rank(n, A, lda, tau);
+  if (nullify) oracle_nullify(n, r, A, lda, V, n);     /* fig:alg_axb line 3 */
   oracle_solve(n, r, A, lda, V, n, B, ldb, k, X, ldx);
   if (rank) *rank = r;
   free(V);
   return ORACLE_OK;
+}
+
+int oracle_lstsq(int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
+                 double* X, int64_t ldx, int64_t nb, int32_t q, double tau, uint64_t seed, int64_t* rank) {
+  return oracle_lstsq_ex(m, n, k, A, lda, B, ldb, X, ldx, nb, q, tau, seed, 0, rank);
 }

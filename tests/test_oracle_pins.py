@@ -328,3 +328,52 @@ def test_threads_bit_identical():
     finally:
         oracle.set_threads(n0)
     assert np.array_equal(X1, X4)
+
+
+# --------------------------------------------------------------------------- Nullify
+def _noisy_gd(m, n, r, tail, seed):
+    """Gd with an exact-rank part plus a small full-rank tail (numerical rank r, no exact gap)."""
+    rng = np.random.default_rng(seed)
+    G = gen.GdMatrix(m, n, r, alpha=2.0, seed=seed)
+    return G.A + tail * rng.standard_normal((m, n)), G
+
+
+def test_nullify_structure_and_exact_rank_invariance():
+    G = gen.GpMatrix(150, 120, 50, seed=41)
+    A = G.A
+    B, _ = G.known_rhs(k=2)
+    out = oracle.randutv(A, 16, 1, seed=3, B=B, want_u=True)
+    r = oracle.rank(out["T"], 1e-10)
+    assert r == 50
+    T2, V2 = oracle.nullify(out["T"], out["V"], r)
+    assert np.all(T2[:r, r:] == 0.0)
+    assert np.all(np.tril(T2[:r, :r], -1) == 0.0)
+    assert np.abs(V2.T @ V2 - np.eye(120)).max() <= 1e-13
+    # exact rank: T22 ~ 0, so A = U T' V'^T still holds
+    assert np.linalg.norm(A - out["U"] @ T2 @ V2.T) <= 1e-13 * np.linalg.norm(A)
+    Xs, rs = oracle.lstsq(A, B, b=16, q=1, seed=3)
+    Xn, rn = oracle.lstsq(A, B, b=16, q=1, seed=3, nullify=True)
+    assert rs == rn and np.linalg.norm(Xs - Xn) <= 1e-12 * np.linalg.norm(Xs)
+
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_nullify_gives_min_norm_solution_of_truncated_factorization(q):
+    """x_nullify = pinv(U_1 [T11 T12] V^T) b (brute force), the min-norm LS solution of the rank-r
+    COD; x_simple only minimises the residual and has a larger norm."""
+    m, n, r, b = 90, 70, 40, 8
+    A, _ = _noisy_gd(m, n, r, 1e-8, seed=43 + q)
+    rng = np.random.default_rng(5)
+    B = rng.standard_normal((m, 1))
+    out = oracle.randutv(A, b, q, seed=2, B=B, want_u=True)
+    rk = oracle.rank(out["T"], 1e-6)
+    assert rk == r
+    T, V, U = out["T"], out["V"], out["U"]
+    Ahat = U[:, :rk] @ T[:rk, :] @ V.T
+    Xref = np.linalg.pinv(Ahat, rcond=1e-12) @ B
+    Xn, rn = oracle.lstsq(A, B, b=b, q=q, tau=1e-6, seed=2, nullify=True)
+    Xs, rs = oracle.lstsq(A, B, b=b, q=q, tau=1e-6, seed=2)
+    assert rn == rs == r
+    assert np.linalg.norm(Xn - Xref) <= 1e-9 * np.linalg.norm(Xref)
+    assert np.linalg.norm(Xn) <= np.linalg.norm(Xs) * (1 + 1e-12)
+    # both minimise the residual of the truncated problem
+    assert np.linalg.norm(Ahat @ Xn - B) == pytest.approx(np.linalg.norm(Ahat @ Xs - B), rel=1e-10)
