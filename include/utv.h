@@ -43,7 +43,7 @@ typedef enum {
 enum {
   UTV_WANT_V = 1u,           /* (informational: V is produced whenever a V pointer is passed) */
   UTV_WANT_U = 2u,           /* build U explicitly (v21t semantics) when U != NULL */
-  UTV_NULLIFY_T12 = 4u,      /* reserved (NEXT): Nullify_top_right_part_of_T, fig:alg_nullify_t12 */
+  UTV_NULLIFY_T12 = 4u,      /* Nullify_top_right_part_of_T after Compute_rank (fig:alg_nullify_t12) */
   UTV_HOST_STREAMED = 8u,    /* reserved (NEXT): out-of-core streaming from pinned host memory */
   UTV_EXPLICIT_V = 16u       /* utv_lstsq: accumulate V explicitly (default: factored V, see below) */
 };
@@ -90,6 +90,10 @@ utv_status utv_synchronize(utv_handle handle);
  *                                 the fly (v23t).
  *   rank                          if non-NULL: r for opts->tau (R10); this reads r back to the
  *                                 host (one synchronisation).
+ * opts->flags & UTV_NULLIFY_T12: after Compute_rank, Nullify_top_right_part_of_T
+ * (fig:alg_nullify_t12) zeroes T(0:r, r:n) by an RZ sweep (blocked, bottom-up, n_b
+ * rows at a time; reading R19) whose reflectors are also applied to V; T(0:r, 0:r) stays upper
+ * triangular but its diagonal blocks are no longer diagonal.  r is computed even if rank is NULL.
  */
 utv_status utv_factor(utv_handle handle, int64_t m, int64_t n, double* A, int64_t lda, double* V,
                       int64_t ldv, double* U, int64_t ldu, double* B, int64_t ldb, int64_t k,
@@ -110,7 +114,10 @@ utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const d
  * (overwritten by T and U^T B); X (n x k) written; *rank = r.  V is not formed: the handle keeps
  * every step's block reflector (W_V, T_V) and V_s (about n^2/2 doubles instead of n^2) and
  * applies V = Q_1 ... Q_s blockdiag(V_s) to [z; 0] (saves the 2 n^3 flops of
- * accumulating V); opts->flags & UTV_EXPLICIT_V accumulates V explicitly instead.  A, B and X may be HOST pointers (pageable or pinned): they are then staged
+ * accumulating V); opts->flags & UTV_EXPLICIT_V accumulates V explicitly instead.  opts->flags & UTV_NULLIFY_T12 runs
+ * Nullify_top_right_part_of_T (fig:alg_nullify_t12, fig:alg_axb line 3 P:1087) after the rank
+ * is known, so X is the minimum-norm solution pinv(A_r) B of the rank-r approximation (the
+ * factored V then also keeps the nullify reflectors, about r (n - r) more doubles).  A, B and X may be HOST pointers (pageable or pinned): they are then staged
  * through device buffers inside the call (the end-to-end path); host A and B are inputs only
  * (left unchanged), a host X is written and the call returns after X has landed.
  */

@@ -63,4 +63,11 @@ void launch_zero_strict_lower(cudaStream_t st, int64_t rows, int64_t cols, doubl
 // flag[0] |= any non-finite entry in A (rows x cols)
 void launch_check_finite(cudaStream_t st, int64_t rows, int64_t cols, const double* A, int64_t lda, int* flag);
 
+// ---- Nullify_top_right_part_of_T helpers (misc.cu) -----------------------------------------
+void launch_rz_build(cudaStream_t st, int64_t bw, int64_t nz, const double* T, int64_t ldt, int64_t i0, int64_t r,
+                     double* M, int64_t ldm);
+void launch_rz_writeback(cudaStream_t st, int64_t bw, int64_t nz, const double* M, int64_t ldm, double* T,
+                         int64_t ldt, int64_t i0, int64_t r);
+void launch_reverse_rows(cudaStream_t st, int64_t bw, const double* src, int64_t lds, double* dst, int64_t ldd);
+
 }  // namespace utv

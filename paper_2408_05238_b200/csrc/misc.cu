@@ -92,3 +92,65 @@ void launch_check_finite(cudaStream_t st, int64_t rows, int64_t cols, const doub
 }
 
 }  // namespace utv
+
+// ---- Nullify_top_right_part_of_T helpers ----------------------------------
+// The RZ factorization of a row slab S = [L | D] (L = T(i0:i0+bw, i0:i0+bw) upper triangular,
+// D = T(i0:i0+bw, r:n)) from the right is a Householder QR of
+//   M = diag(J, I) S^T J     (J = exchange matrix),
+// whose top bw x bw block is upper triangular, so each reflector touches exactly one top row and
+// the D rows: the RZ structure.  S C = [J R^T J, 0] with C = I - W' T W'^T, W' = diag(J, I) W.
+namespace utv {
+namespace {
+__global__ void rz_build_kernel(int64_t bw, int64_t nz, const double* __restrict__ T, int64_t ldt, int64_t i0,
+                                int64_t r, double* __restrict__ M, int64_t ldm) {
+  const int64_t rows = bw + nz, total = rows * bw;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e % rows, q = e / rows;
+    const int64_t srow = i0 + bw - 1 - q;
+    M[cm(p, q, ldm)] = p < bw ? T[cm(srow, i0 + bw - 1 - p, ldt)] : T[cm(srow, r + (p - bw), ldt)];
+  }
+}
+// T(i0:i0+bw, i0:i0+bw) = J R^T J (R = upper bw x bw of M), T(i0:i0+bw, r:n) = 0
+__global__ void rz_writeback_kernel(int64_t bw, int64_t nz, const double* __restrict__ M, int64_t ldm,
+                                    double* __restrict__ T, int64_t ldt, int64_t i0, int64_t r) {
+  const int64_t total = bw * (bw + nz);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e % bw, c = e / bw;
+    if (c < bw) {
+      const int64_t pr = bw - 1 - c, pc = bw - 1 - a;      // R(pr, pc), upper: pr <= pc  <=>  a <= c
+      T[cm(i0 + a, i0 + c, ldt)] = pr <= pc ? M[cm(pr, pc, ldm)] : 0.0;
+    } else {
+      T[cm(i0 + a, r + (c - bw), ldt)] = 0.0;
+    }
+  }
+}
+// dst (bw x bw) = J * src(0:bw, 0:bw)  (row reversal of the top block of W)
+__global__ void reverse_rows_kernel(int64_t bw, const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                                    int64_t ldd) {
+  const int64_t total = bw * bw;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e % bw, q = e / bw;
+    dst[cm(p, q, ldd)] = src[cm(bw - 1 - p, q, lds)];
+  }
+}
+int grid_for2(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16)); }
+}  // namespace
+
+void launch_rz_build(cudaStream_t st, int64_t bw, int64_t nz, const double* T, int64_t ldt, int64_t i0, int64_t r,
+                     double* M, int64_t ldm) {
+  ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)bw * (bw + nz));
+  rz_build_kernel<<<grid_for2(bw * (bw + nz)), 256, 0, st>>>(bw, nz, T, ldt, i0, r, M, ldm);
+  UTV_CUDA(cudaGetLastError());
+}
+void launch_rz_writeback(cudaStream_t st, int64_t bw, int64_t nz, const double* M, int64_t ldm, double* T,
+                         int64_t ldt, int64_t i0, int64_t r) {
+  ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)bw * (bw + nz));
+  rz_writeback_kernel<<<grid_for2(bw * (bw + nz)), 256, 0, st>>>(bw, nz, M, ldm, T, ldt, i0, r);
+  UTV_CUDA(cudaGetLastError());
+}
+void launch_reverse_rows(cudaStream_t st, int64_t bw, const double* src, int64_t lds, double* dst, int64_t ldd) {
+  ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)bw * bw);
+  reverse_rows_kernel<<<grid_for2(bw * bw), 256, 0, st>>>(bw, src, lds, dst, ldd);
+  UTV_CUDA(cudaGetLastError());
+}
+}  // namespace utv

@@ -34,6 +34,7 @@ struct utv_handle_s {
   // lstsq buffers
   double* vbuf = nullptr; size_t vbuf_doubles = 0;
   double* stage = nullptr; size_t stage_doubles = 0;   // host-pointer staging (A, B, X)
+  double* nbuf = nullptr; size_t nbuf_doubles = 0;     // factored Nullify blocks (C_1..C_p)
   Profiler prof;
 };
 
@@ -91,6 +92,7 @@ struct Layout {
   size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, S, Tu, tauu, Z1, Z2, tmp, R, Us, Vs, sig;
   size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve;
   size_t part2, pz1b, pz2b, gram2, px2, gemm2, tmp2;
+  size_t nM, nW, ntau, nT, nWt, nY, nY2;
   size_t gemm_doubles, gemm2_doubles;
   size_t total;
 };
@@ -147,6 +149,14 @@ Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
   L.gemm2_doubles = std::max<size_t>((size_t)128 * b * std::max<int64_t>(b, 32), (size_t)1 << 20);
   L.gemm2 = take(L.gemm2_doubles);
   L.tmp2 = take(std::max<size_t>(mx * b, (size_t)b * nk));
+  // Nullify_top_right_part_of_T (only touched when UTV_NULLIFY_T12 is set)
+  L.nM = take((size_t)(b + n) * b);
+  L.nW = take((size_t)(b + n) * b);
+  L.ntau = take(b);
+  L.nT = take((size_t)b * b);
+  L.nWt = take((size_t)b * b);
+  L.nY = take(std::max<size_t>(mx * b, (size_t)n * std::max<int64_t>(k, 1)));
+  L.nY2 = take(mx * b);
   L.total = off;
   return L;
 }
@@ -395,9 +405,68 @@ void solve_impl(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t ldt
   c.gemm(false, false, n, k, r, 1.0, V, ldv, Zb, r, 0.0, X, ldx);
 }
 
-// X = V(:, 0:r) z with V in factored form: X = Q_1 ... Q_s D [z; 0]  (X is n x k, ldx).
+// Nullify_top_right_part_of_T (fig:alg_nullify_t12), blocked bottom-up
+// in row blocks of b: for rows i0:i1 the RZ factorization of the slab [T(i0:i1, i0:i1) | T(i0:i1, r:n)]
+// is the Householder QR of M = diag(J, I) S^T J (panel_qr, same dlarfg conventions as the oracle's
+// row-by-row sweep), giving S C = [J R^T J, 0] with C = I - W' T_z W'^T, W' = diag(J, I) W; C is
+// applied to the rows above ("Update(C11, D1, C01, D0)") and to V ("Update(C11, D1, E1, F)") as
+// DMMA GEMMs over the two column ranges (i0:i1) and (r:n).  With V factored, C is kept (ns).
+struct NullStore {
+  double* Wtop = nullptr;   // per block q: b x b (ld b)      W'_top = J W_top
+  double* Wbot = nullptr;   // per block q: nz x b (ld nz)    W'_bot
+  double* Tz = nullptr;     // per block q: b x b (ld b)
+  std::vector<int64_t> i0, bw;
+  int64_t nz = 0;
+};
+
+void nullify_impl(const Ctx& c, int64_t n, int64_t r, double* T, int64_t ldt, double* V, int64_t ldv, int64_t b,
+                  NullStore* ns) {
+  const int64_t nz = n - r;
+  if (nz <= 0 || r <= 0) return;
+  cudaStream_t st = c.st;
+  const int64_t ldm = b + nz;
+  double *M = c.at(c.L.nM), *W = c.at(c.L.nW), *tz = c.at(c.L.ntau), *Tz = c.at(c.L.nT), *Wt = c.at(c.L.nWt);
+  double *Y = c.at(c.L.nY), *Y2 = c.at(c.L.nY2);
+  if (ns) ns->nz = nz;
+  for (int64_t i1 = r, q = 0; i1 > 0; ++q) {
+    const int64_t i0 = std::max<int64_t>(0, i1 - b), bw = i1 - i0;
+    launch_rz_build(st, bw, nz, T, ldt, i0, r, M, ldm);
+    panel_qr(st, bw + nz, bw, M, ldm, W, ldm, tz, Tz, b, c.pw);
+    launch_rz_writeback(st, bw, nz, M, ldm, T, ldt, i0, r);
+    launch_reverse_rows(st, bw, W, ldm, Wt, b);
+    const double* Wb = W + bw;                                           // W'_bot (ld ldm)
+    auto apply_rows = [&](double* X, int64_t ldx, int64_t rows) {        // X(:, cols) <- X(:, cols) C
+      double* Xl = X + cm(0, i0, ldx);
+      double* Xr = X + cm(0, r, ldx);
+      c.gemm(false, false, rows, bw, bw, 1.0, Xl, ldx, Wt, b, 0.0, Y, rows);
+      c.gemm(false, false, rows, bw, nz, 1.0, Xr, ldx, Wb, ldm, 1.0, Y, rows);
+      c.gemm(false, false, rows, bw, bw, 1.0, Y, rows, Tz, b, 0.0, Y2, rows);
+      c.gemm(false, true, rows, bw, bw, -1.0, Y2, rows, Wt, b, 1.0, Xl, ldx);
+      c.gemm(false, true, rows, nz, bw, -1.0, Y2, rows, Wb, ldm, 1.0, Xr, ldx);
+    };
+    if (i0 > 0) apply_rows(T, ldt, i0);                                  // rows above
+    if (V) apply_rows(V, ldv, n);
+    if (ns) {
+      launch_copy(st, bw, bw, Wt, b, ns->Wtop + (size_t)q * b * b, b);
+      launch_copy(st, nz, bw, Wb, ldm, ns->Wbot + (size_t)q * nz * b, nz);
+      launch_copy(st, bw, bw, Tz, b, ns->Tz + (size_t)q * b * b, b);
+      ns->i0.push_back(i0);
+      ns->bw.push_back(bw);
+    }
+    i1 = i0;
+  }
+}
+
+size_t null_store_doubles(int64_t n, int64_t r, int64_t b) {
+  if (r <= 0 || n - r <= 0) return 0;
+  const size_t nblk = (size_t)((r + b - 1) / b);
+  return nblk * ((size_t)(n - r) * b + 2 * (size_t)b * b);
+}
+
+// X = V(:, 0:r) z with V in factored form: X = Q_1 ... Q_s D [C_1 ... C_p] [z; 0]  (X is n x k).
 void solve_factored(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t ldt, const double* Cm, int64_t ldc,
-                    int64_t k, double* X, int64_t ldx, const FactoredV& fv, int64_t b) {
+                    int64_t k, double* X, int64_t ldx, const FactoredV& fv, int64_t b,
+                    const NullStore* ns = nullptr) {
   cudaStream_t st = c.st;
   if (k <= 0) return;
   launch_set_zero(st, n, k, X, ldx);
@@ -412,9 +481,32 @@ void solve_factored(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t
   }
   double* tmp = c.at(c.L.Z1);
   double* tmp2 = c.at(c.L.Z2);
-  for (int64_t j0 = 0, step = 0; j0 < r; j0 += b, ++step) {                  // D: X(blk) = V_s,i z(blk)
-    const int64_t bw = std::min(b, n - j0), zr = std::min(bw, r - j0);
-    c.gemm(false, false, bw, k, zr, 1.0, fv.Vs + (size_t)step * b * b, b, Zb + j0, r, 0.0, X + j0, ldx);
+  const bool nul = ns && !ns->i0.empty();
+  if (!nul) {
+    for (int64_t j0 = 0, step = 0; j0 < r; j0 += b, ++step) {                // D: X(blk) = V_s,i z(blk)
+      const int64_t bw = std::min(b, n - j0), zr = std::min(bw, r - j0);
+      c.gemm(false, false, bw, k, zr, 1.0, fv.Vs + (size_t)step * b * b, b, Zb + j0, r, 0.0, X + j0, ldx);
+    }
+  } else {
+    // y = C_1 ... C_p [z; 0] (the last-processed nullify block first), then D on every block
+    double* Yv = c.at(c.L.nY);                                            // n x k
+    launch_set_zero(st, n, k, Yv, n);
+    launch_copy(st, r, k, Zb, r, Yv, n);
+    const int64_t nz = ns->nz;
+    for (int64_t q = (int64_t)ns->i0.size() - 1; q >= 0; --q) {
+      const int64_t i0 = ns->i0[q], bw = ns->bw[q];
+      const double* Wt = ns->Wtop + (size_t)q * b * b;
+      const double* Wb = ns->Wbot + (size_t)q * nz * b;
+      c.gemm(true, false, bw, k, bw, 1.0, Wt, b, Yv + i0, n, 0.0, tmp, b);
+      c.gemm(true, false, bw, k, nz, 1.0, Wb, nz, Yv + r, n, 1.0, tmp, b);
+      c.gemm(false, false, bw, k, bw, 1.0, ns->Tz + (size_t)q * b * b, b, tmp, b, 0.0, tmp2, b);
+      c.gemm(false, false, bw, k, bw, -1.0, Wt, b, tmp2, b, 1.0, Yv + i0, n);
+      c.gemm(false, false, nz, k, bw, -1.0, Wb, nz, tmp2, b, 1.0, Yv + r, n);
+    }
+    for (int64_t j0 = 0, step = 0; j0 < n; j0 += b, ++step) {                // D on all blocks
+      const int64_t bw = std::min(b, n - j0);
+      c.gemm(false, false, bw, k, bw, 1.0, fv.Vs + (size_t)step * b * b, b, Yv + j0, n, 0.0, X + j0, ldx);
+    }
   }
   for (int64_t i = (int64_t)fv.woff.size() - 1; i >= 0; --i) {                // X = Q_i X, i = s..1
     const int64_t j0 = fv.j0[i], np = fv.np[i];
@@ -488,7 +580,7 @@ utv_status utv_destroy(utv_handle h) {
   if (h->ev_svd) cudaEventDestroy(h->ev_svd);
   cudaFree(h->bar2);
   cudaFree(h->ws); cudaFree(h->bar); cudaFree(h->info); cudaFree(h->flag); cudaFree(h->d_rank);
-  cudaFree(h->vbuf); cudaFree(h->stage);
+  cudaFree(h->vbuf); cudaFree(h->stage); cudaFree(h->nbuf);
   cudaFreeHost(h->h_rank); cudaFreeHost(h->h_info);
   cudaGetLastError();
   delete h;
@@ -520,7 +612,9 @@ utv_status utv_factor(utv_handle h, int64_t m, int64_t n, double* A, int64_t lda
     if (n == 0) { if (rank) *rank = 0; return; }
     Ctx c = make_ctx(h, m, n, k, opts->block);
     factor_impl(c, m, n, A, lda, V, ldv, want_u ? U : nullptr, ldu, (B && k > 0) ? B : nullptr, ldb, k, *opts);
-    int64_t r = finish_factor(c, n, A, lda, opts->tau, rank != nullptr);
+    const bool nullify = (opts->flags & UTV_NULLIFY_T12) != 0;
+    int64_t r = finish_factor(c, n, A, lda, opts->tau, rank != nullptr || nullify);
+    if (nullify) nullify_impl(c, n, r, A, lda, V, ldv, opts->block, nullptr);   // fig:alg_axb line 3
     if (rank) *rank = r;
   });
 }
@@ -562,7 +656,9 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     if (hX) { dX = h->stage + off; dldx = n; off += (size_t)n * k; }
     const int64_t b = opts->block;
     const bool explicit_v = (opts->flags & UTV_EXPLICIT_V) != 0;
+    const bool nullify = (opts->flags & UTV_NULLIFY_T12) != 0;
     FactoredV fv;
+    NullStore ns;
     if (explicit_v) {
       ensure_buf(&h->vbuf, &h->vbuf_doubles, (size_t)n * n);
     } else {
@@ -577,9 +673,17 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     else
       factor_impl(c, m, n, dA, dlda, nullptr, 0, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts, &fv);
     int64_t r = finish_factor(c, n, dA, dlda, opts->tau, true);
+    if (nullify) {                                                     // fig:alg_axb line 3
+      if (!explicit_v) {
+        ensure_buf(&h->nbuf, &h->nbuf_doubles, null_store_doubles(n, r, b) + 64);
+        const size_t nblk = (size_t)((r + b - 1) / b);
+        ns.Wtop = h->nbuf; ns.Tz = h->nbuf + nblk * b * b; ns.Wbot = ns.Tz + nblk * b * b;
+      }
+      nullify_impl(c, n, r, dA, dlda, explicit_v ? h->vbuf : nullptr, n, b, explicit_v ? nullptr : &ns);
+    }
     if (k > 0) {
       if (explicit_v) solve_impl(c, n, r, dA, dlda, h->vbuf, n, dB, dldb, k, dX, dldx);
-      else solve_factored(c, n, r, dA, dlda, dB, dldb, k, dX, dldx, fv, b);
+      else solve_factored(c, n, r, dA, dlda, dB, dldb, k, dX, dldx, fv, b, nullify ? &ns : nullptr);
     }
     // host A / B are inputs only: they are not written back (see utv.h)
     if (hX) copy2d(st, X, ldx, dX, n, n, k, cudaMemcpyDeviceToHost);
