@@ -353,7 +353,7 @@ def run_ours(args):
         "v_mode": "factored (SURVEY 8(f) #4)" if factored else "explicit",
         "frac_of_fp64_peak": executed_tflops / (world * peak),
         "fp64_peak_tflops": peak, "f_alg": F, "rank": r, "rank_ok": r == r_true, "rel_err_x0": rel_err,
-        "roofline": {"kernel": "dgemm_dmma_kernel (FP64 mma.sync DMMA, all GEMM launches of the step)",
+        "roofline": {"kernel": "dgemm_tma_kernel (TMA-fed FP64 mma.sync DMMA; all GEMM launches of the step)",
                      "bound": "tensor", "achieved": gemm_tf, "peak": peak, "unit": "TFLOP/s",
                      "frac": (gemm_tf / peak) if gemm_tf else None, "traffic": None,
                      "peak_source": peak_src,

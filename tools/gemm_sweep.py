@@ -24,5 +24,6 @@ for n in (50000, 25000):
     t_gemm(f"NT_update_{n}x{n}_K256", False, True, n, n, 256, beta=1.0)
     t_gemm(f"TN_256x{n}_K{n}", True, False, 256, n, n)
     t_gemm(f"NN_update_{n}x{n}_K256", False, False, n, n, 256, beta=1.0)
+    t_gemm(f"NT_update_{n}x{n}_K512", False, True, n, n, 512, beta=1.0)
 t_gemm("square_8192", False, False, 8192, 8192, 8192)
-json.dump(res, open(f"gpurun_out/gemm_sweep_{os.environ.get('UTV_GEMM_WN', 'auto')}.json", "w"), indent=1)
+json.dump(res, open(f"gpurun_out/gemm_sweep_{os.environ.get('TAG', 'auto')}.json", "w"), indent=1)
