@@ -44,7 +44,7 @@ enum {
   UTV_WANT_V = 1u,           /* (informational: V is produced whenever a V pointer is passed) */
   UTV_WANT_U = 2u,           /* build U explicitly (v21t semantics) when U != NULL */
   UTV_NULLIFY_T12 = 4u,      /* Nullify_top_right_part_of_T after Compute_rank (fig:alg_nullify_t12) */
-  UTV_HOST_STREAMED = 8u,    /* reserved (NEXT): out-of-core streaming from pinned host memory */
+  UTV_HOST_STREAMED = 8u,    /* utv_lstsq: A stays in host memory, streamed through HBM (out of core) */
   UTV_EXPLICIT_V = 16u       /* utv_lstsq: accumulate V explicitly (default: factored V, see below) */
 };
 
@@ -124,6 +124,26 @@ utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const d
 utv_status utv_lstsq(utv_handle handle, int64_t m, int64_t n, int64_t k, double* A, int64_t lda,
                      double* B, int64_t ldb, double* X, int64_t ldx, const utv_opts* opts,
                      int64_t* rank);
+
+/*
+ * Out-of-core mode (opts->flags & UTV_HOST_STREAMED; the paper's out-of-core regime, P:1580-1675,
+ * P:1790-1824) -- utv_lstsq only, fast option with factored V (UTV_NULLIFY_T12 /
+ * UTV_EXPLICIT_V -> UTV_ERR_UNSUPPORTED).  A must be a HOST pointer (pinned or pageable; pageable
+ * memory is registered with cudaHostRegister for the duration of the call) and is OVERWRITTEN by T
+ * there.  B and X may be host or device pointers (a device B is overwritten by U^T B, a host B is
+ * left unchanged).  HBM holds the workspace, the factored V (about n^2/2 doubles), a ring of staging
+ * chunks and as many trailing column blocks as the device budget allows; the other column blocks
+ * are streamed host <-> device on two copy streams, overlapped with the GEMMs (2q+2 reads and one
+ * write of the trailing columns per step).  UTV_ERR_ALLOC if the budget cannot hold the fixed part.
+ */
+/* Device-memory budget in bytes for UTV_HOST_STREAMED calls on this handle (workspace + factored V
+ * + staging + resident blocks); 0 (default) = free HBM at call time minus 1 GiB. */
+utv_status utv_set_device_budget(utv_handle handle, int64_t bytes);
+
+/* Host-link traffic of the last UTV_HOST_STREAMED call: bytes copied host->device and
+ * device->host, and the number of trailing columns that were kept resident in HBM. */
+utv_status utv_stream_stats(utv_handle handle, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                            int64_t* resident_cols);
 
 /* Library version string, e.g. "utv-b200 0.1 sm_100a". */
 const char* utv_version(void);

@@ -27,7 +27,7 @@ EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "u
             "utv_factor", "utv_solve", "utv_lstsq", "utv_version", "utv_sketch", "utv_philox", "utv_hqr",
             "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read",
             "utv_profile_dump", "utv_svd_block", "utv_svd_status", "utv_trsm_upper",
-            "utv_rank_diag"]
+            "utv_rank_diag", "utv_set_device_budget", "utv_stream_stats"]
 PROF_FAMILIES = ["gemm", "panel", "svd", "sketch", "solve", "misc"]
 
 
@@ -96,6 +96,8 @@ def lib() -> C.CDLL:
             "utv_svd_status": ([p, C.POINTER(i32), C.POINTER(i32)], st),
             "utv_trsm_upper": ([p, i64, p, i64, p, i64, i64], st),
             "utv_rank_diag": ([p, i64, p, d, C.POINTER(i64)], st),
+            "utv_set_device_budget": ([p, i64], st),
+            "utv_stream_stats": ([p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], st),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -216,6 +218,16 @@ class Handle:
         self.check(lib().utv_lstsq(self.h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(X), _ld(X), C.byref(o),
                                    C.byref(r)))
         return int(r.value)
+
+    def set_device_budget(self, nbytes: int):
+        """HBM budget (bytes) of UTV_HOST_STREAMED calls; 0 = free HBM minus 1 GiB."""
+        self.check(lib().utv_set_device_budget(self.h, int(nbytes)))
+
+    def stream_stats(self) -> dict:
+        """Host-link traffic of the last UTV_HOST_STREAMED call."""
+        a, b, c = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        self.check(lib().utv_stream_stats(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"h2d_bytes": int(a.value), "d2h_bytes": int(b.value), "resident_cols": int(c.value)}
 
     # ------------------------------------------------------------------ step entry points
     def sketch(self, seed: int, step: int, row0: int, mrows: int, b: int, G=None):

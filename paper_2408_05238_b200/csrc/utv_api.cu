@@ -1,6 +1,7 @@
 // utv_api.cu -- the C ABI of libutv.so (include/utv.h, include/utv_steps.h) and the host
 // orchestration of randUTV on one B200: the per-step launch sequence of fig:alg_utv
 // over the sm_100a kernels, the handle's workspace arena and error mapping.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -35,6 +36,13 @@ struct utv_handle_s {
   double* vbuf = nullptr; size_t vbuf_doubles = 0;
   double* stage = nullptr; size_t stage_doubles = 0;   // host-pointer staging (A, B, X)
   double* nbuf = nullptr; size_t nbuf_doubles = 0;     // factored Nullify blocks (C_1..C_p)
+  // out-of-core streaming (UTV_HOST_STREAMED)
+  double* ooc = nullptr; size_t ooc_doubles = 0;       // resident column blocks + staging + panel
+  int64_t dev_budget = 0;                              // bytes; 0 = free HBM at call time - 1 GiB
+  int64_t ooc_h2d = 0, ooc_d2h = 0, ooc_resident_cols = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  static constexpr int kStg = 3;
+  cudaEvent_t ev_loaded[kStg] = {}, ev_free[kStg] = {}, ev_done = nullptr, ev_wb = nullptr;
   Profiler prof;
 };
 
@@ -464,20 +472,24 @@ size_t null_store_doubles(int64_t n, int64_t r, int64_t b) {
 }
 
 // X = V(:, 0:r) z with V in factored form: X = Q_1 ... Q_s D [C_1 ... C_p] [z; 0]  (X is n x k).
+// z_ready: z = T11^{-1} C(0:r) is already in the zsolve buffer (ld r; the streamed path solves it
+// block by block as T's columns arrive) -- T and Cm are then not read.
 void solve_factored(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t ldt, const double* Cm, int64_t ldc,
                     int64_t k, double* X, int64_t ldx, const FactoredV& fv, int64_t b,
-                    const NullStore* ns = nullptr) {
+                    const NullStore* ns = nullptr, bool z_ready = false) {
   cudaStream_t st = c.st;
   if (k <= 0) return;
   launch_set_zero(st, n, k, X, ldx);
   if (r <= 0) return;
   double* Zb = c.at(c.L.zsolve);
-  launch_copy(st, r, k, Cm, ldc, Zb, r);
-  constexpr int64_t SB = 256;
-  for (int64_t j0 = ((r - 1) / SB) * SB; j0 >= 0; j0 -= SB) {                 // z = T11^{-1} C(0:r)
-    const int64_t j1 = std::min(r, j0 + SB);
-    launch_trsv_block(st, j0, j1, T, ldt, Zb, r, k);
-    if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Zb + j0, r, 1.0, Zb, r);
+  if (!z_ready) {
+    launch_copy(st, r, k, Cm, ldc, Zb, r);
+    constexpr int64_t SB = 256;
+    for (int64_t j0 = ((r - 1) / SB) * SB; j0 >= 0; j0 -= SB) {               // z = T11^{-1} C(0:r)
+      const int64_t j1 = std::min(r, j0 + SB);
+      launch_trsv_block(st, j0, j1, T, ldt, Zb, r, k);
+      if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Zb + j0, r, 1.0, Zb, r);
+    }
   }
   double* tmp = c.at(c.L.Z1);
   double* tmp2 = c.at(c.L.Z2);
@@ -517,11 +529,324 @@ void solve_factored(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Out-of-core randUTV (UTV_HOST_STREAMED, the paper's out-of-core regime
+// P:1580-1675).  A stays in (pinned) host memory and is overwritten by T there.
+// HBM holds the workspace, the factored V, a staging ring of kStg chunks (cw columns, all rows)
+// and as many trailing column blocks as the device budget allows: columns [c_res, n) are loaded
+// once and stay resident (the last blocks are the ones every step touches); columns < c_res are
+// streamed H2D on one copy stream and D2H on another, overlapped with the DMMA GEMMs of the
+// previous / next chunk (the column-block decomposition of every product is exact).  Per step:
+//   passes over the trailing columns, rows j0:m:  Z = A'Y (accumulated), Y = A'^T Z   (q times)
+//   QR(Y) -> W_V, T_V;  pass, all rows:  X = A W_V (accumulated);  X2 = X T_V
+//   block i (loaded): right update, panel QR, SVD, written back
+//   one read+write pass over the columns > i:  right update (all rows), Q_U^T (rows j0:m),
+//   U_s^T (rows j0:j0+b), and the NEXT step's sketch product Y' = A''^T G' (rows j0+b:m,
+//   which the U_s^T update does not touch) -- so each step streams 2q+2 reads + 1 write.
+// ------------------------------------------------------------------------------------------
+struct Ooc {
+  utv_handle h = nullptr;
+  int64_t m = 0, n = 0, b = 0;
+  double* hA = nullptr;
+  int64_t lda = 0;
+  int64_t c_res = 0;      // first resident column (multiple of b)
+  double* res = nullptr;  // device, m x (n - c_res), ld m
+  int64_t cw = 0;         // staging chunk width (columns, multiple of b)
+  double* stg[utv_handle_s::kStg] = {};
+  double* pb = nullptr;   // device m x b: the step's own block column when it is streamed
+  int next = 0;
+};
+
+// h2d waits for every write-back enqueued so far (host data consistency).
+void ooc_sync_wb(Ooc& o) {
+  UTV_CUDA(cudaEventRecord(o.h->ev_wb, o.h->d2h));
+  UTV_CUDA(cudaStreamWaitEvent(o.h->h2d, o.h->ev_wb, 0));
+}
+
+// Enqueue a host -> device copy on h2d and make the main stream wait for it.
+void ooc_load(Ooc& o, const Ctx& c, double* dst, int64_t ldd, int64_t row0, int64_t rows, int64_t col, int64_t w,
+              cudaEvent_t done) {
+  utv_handle h = o.h;
+  copy2d(h->h2d, dst, ldd, o.hA + cm(row0, col, o.lda), o.lda, rows, w, cudaMemcpyHostToDevice);
+  h->ooc_h2d += rows * w * 8;
+  UTV_CUDA(cudaEventRecord(done, h->h2d));
+  UTV_CUDA(cudaStreamWaitEvent(c.st, done, 0));
+}
+
+void ooc_store(Ooc& o, const Ctx& c, const double* src, int64_t lds, int64_t row0, int64_t rows, int64_t col,
+               int64_t w, cudaEvent_t done) {
+  utv_handle h = o.h;
+  UTV_CUDA(cudaEventRecord(h->ev_done, c.st));
+  UTV_CUDA(cudaStreamWaitEvent(h->d2h, h->ev_done, 0));
+  copy2d(h->d2h, o.hA + cm(row0, col, o.lda), o.lda, src, lds, rows, w, cudaMemcpyDeviceToHost);
+  h->ooc_d2h += rows * w * 8;
+  if (done) UTV_CUDA(cudaEventRecord(done, h->d2h));
+}
+
+// One pass over columns [c0, n), rows row0:m: fn(dev, ld, col, w) on the main stream with dev at
+// (row0, col).  Resident columns first (one call), then the streamed chunks through the ring.
+template <typename F>
+void ooc_pass(Ooc& o, const Ctx& c, int64_t c0, int64_t row0, bool write_back, F&& fn) {
+  utv_handle h = o.h;
+  const int64_t rows = o.m - row0;
+  const int64_t r0 = std::max(c0, o.c_res);
+  if (r0 < o.n) fn(o.res + cm(row0, r0 - o.c_res, o.m), o.m, r0, o.n - r0);
+  // chunks of one pass are disjoint, so only earlier passes' write-backs must land first
+  if (c0 < std::min(o.n, o.c_res)) ooc_sync_wb(o);
+  for (int64_t col = c0; col < std::min(o.n, o.c_res); col += o.cw) {
+    const int64_t w = std::min(o.cw, o.c_res - col);
+    const int s = o.next;
+    o.next = (o.next + 1) % utv_handle_s::kStg;
+    double* d = o.stg[s];
+    UTV_CUDA(cudaStreamWaitEvent(h->h2d, h->ev_free[s], 0));          // slot's previous chunk done
+    ooc_load(o, c, d, o.m, row0, rows, col, w, h->ev_loaded[s]);
+    fn(d, o.m, col, w);
+    if (write_back) {
+      ooc_store(o, c, d, o.m, row0, rows, col, w, h->ev_free[s]);
+    } else {
+      UTV_CUDA(cudaEventRecord(h->ev_free[s], c.st));
+    }
+  }
+}
+
+// Device pointer (row 0, ld *ld) of the column block [j0, j0 + w), rows 0:rows loaded if streamed.
+double* ooc_block(Ooc& o, const Ctx& c, int64_t j0, int64_t w, int64_t rows, int64_t* ld) {
+  *ld = o.m;
+  if (j0 >= o.c_res) return o.res + cm(0, j0 - o.c_res, o.m);
+  UTV_CUDA(cudaEventRecord(o.h->ev_done, c.st));                      // pb's previous readers
+  UTV_CUDA(cudaStreamWaitEvent(o.h->h2d, o.h->ev_done, 0));
+  ooc_sync_wb(o);
+  ooc_load(o, c, o.pb, o.m, 0, rows, j0, w, o.h->ev_loaded[0]);
+  return o.pb;
+}
+
+void ooc_block_store(Ooc& o, const Ctx& c, int64_t j0, int64_t w) {
+  if (j0 >= o.c_res) return;
+  ooc_store(o, c, o.pb, o.m, 0, o.m, j0, w, nullptr);
+}
+
+// diag(T) is gathered into dg (n) as each block's sigma is set; C (device, ldc) becomes U^T B.
+void factor_ooc(const Ctx& c, Ooc& o, double* Cd, int64_t ldc, int64_t k, const utv_opts& opt, FactoredV* fv,
+                double* dg) {
+  cudaStream_t st = c.st;
+  const Layout& L = c.L;
+  const int64_t b = opt.block, m = o.m, n = o.n;
+  const int ns = c.h->num_sms;
+  UTV_CUDA(cudaMemsetAsync(c.h->info, 0, 4 * sizeof(int), st));
+  UTV_CUDA(cudaMemsetAsync(c.h->flag, 0, sizeof(int), st));
+  if (Cd && k > 0) launch_check_finite(st, m, k, Cd, ldc, c.h->flag);
+  double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *WV = c.at(L.Wv), *tauv = c.at(L.tauv);
+  double *X = c.at(L.X), *X2 = c.at(L.X2), *Wu = c.at(L.Wu), *Tu = c.at(L.Tu), *tauu = c.at(L.tauu);
+  double *Z1 = c.at(L.Z1), *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp2), *Us = c.at(L.Us), *sig = c.at(L.sig);
+  // resident columns: loaded once
+  if (o.c_res < n) {
+    UTV_CUDA(cudaEventRecord(o.h->ev_done, st));
+    UTV_CUDA(cudaStreamWaitEvent(o.h->h2d, o.h->ev_done, 0));
+    ooc_load(o, c, o.res, m, 0, m, o.c_res, n - o.c_res, o.h->ev_loaded[0]);
+    launch_check_finite(st, m, n - o.c_res, o.res, m, c.h->flag);
+  }
+  bool y_ready = false;
+  for (int64_t j0 = 0, step = 0; j0 < n; j0 += b, ++step) {
+    const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0, nr = np - bw;
+    const bool right = np > b;                                                     // R5
+    double* Tvs = fv->T + (size_t)step * b * b;
+    if (right) {
+      if (!y_ready) {                                                              // a1 + Y = A'^T G
+        launch_sketch(st, opt.seed, step, j0, mp, b, G, mp, ns);
+        ooc_pass(o, c, j0, j0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+          if (step == 0 && col < o.c_res) launch_check_finite(st, mp, w, d, ld, c.h->flag);
+          c.gemm(true, false, w, b, mp, 1.0, d, ld, G, mp, 0.0, Y + (col - j0), np);
+        });
+      }
+      for (int32_t it = 0; it < opt.power_iters; ++it) {                          // a2 (R7)
+        launch_set_zero(st, mp, b, Z, mp);
+        ooc_pass(o, c, j0, j0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+          c.gemm(false, false, mp, b, w, 1.0, d, ld, Y + (col - j0), np, 1.0, Z, mp);
+        });
+        ooc_pass(o, c, j0, j0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+          c.gemm(true, false, w, b, mp, 1.0, d, ld, Z, mp, 0.0, Y + (col - j0), np);
+        });
+      }
+      panel_qr(st, np, b, Y, np, WV, np, tauv, Tvs, b, c.pw);                     // a3
+      fv->woff.push_back(fv->woff.empty() ? 0 : fv->woff.back() + (size_t)fv->np.back() * b);
+      fv->j0.push_back(j0); fv->np.push_back(np); fv->has_q.push_back(1);
+      launch_copy(st, np, b, WV, np, fv->W + fv->woff.back(), np);
+      launch_set_zero(st, m, b, X, m);                                             // a4, R1: all rows
+      ooc_pass(o, c, j0, 0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+        c.gemm(false, false, m, b, w, 1.0, d, ld, WV + (col - j0), np, 1.0, X, m);
+      });
+      c.gemm(false, false, m, b, b, 1.0, X, m, Tvs, b, 0.0, X2, m);
+    }
+    // ---- block i: right update, panel QR (a5), C := Q_U^T C, SVD and its updates (a7)
+    int64_t lda_i = m;
+    double* Ai = ooc_block(o, c, j0, bw, m, &lda_i);
+    if (right) c.gemm(false, true, m, bw, b, -1.0, X2, m, WV, np, 1.0, Ai, lda_i);
+    panel_qr(st, mp, bw, Ai + j0, lda_i, Wu, m, tauu, Tu, b, c.pw);
+    if (Cd && k > 0) {
+      double* Cr = Cd + j0;
+      c.gemm(true, false, bw, k, mp, 1.0, Wu, m, Cr, ldc, 0.0, Z1, bw);
+      c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+      c.gemm(false, false, mp, k, bw, -1.0, Wu, m, Z2, bw, 1.0, Cr, ldc);
+    }
+    double* Vsi = fv->Vs + (size_t)step * b * b;
+    svd_small(st, bw, Ai + j0, lda_i, Us, b, sig, Vsi, b, c.sw);
+    launch_set_diag(st, bw, sig, Ai + j0, lda_i);
+    launch_copy(st, bw, 1, sig, bw, dg + j0, n);
+    if (j0 > 0) {                                                                  // A01 := A01 V_s
+      c.gemm(false, false, j0, bw, bw, 1.0, Ai, lda_i, Vsi, b, 0.0, tmp, j0);
+      launch_copy(st, j0, bw, tmp, j0, Ai, lda_i);
+    }
+    if (Cd && k > 0) {                                                             // C1 := U_s^T C1
+      c.gemm(true, false, bw, k, bw, 1.0, Us, b, Cd + j0, ldc, 0.0, Z1, bw);
+      launch_copy(st, bw, k, Z1, bw, Cd + j0, ldc);
+    }
+    ooc_block_store(o, c, j0, bw);
+    // ---- one read+write pass over the trailing columns (+ the next step's sketch product)
+    if (nr > 0) {
+      const bool next_sketch = nr > b;
+      if (next_sketch) launch_sketch(st, opt.seed, step + 1, j0 + b, mp - b, b, G, mp - b, ns);
+      ooc_pass(o, c, j0 + bw, 0, true, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+        if (right) c.gemm(false, true, m, w, b, -1.0, X2, m, WV + (col - j0), np, 1.0, d, ld);
+        double* dr = d + j0;                                                       // a6, R3
+        c.gemm(true, false, bw, w, mp, 1.0, Wu, m, dr, ld, 0.0, Z1, bw);
+        c.gemm(true, false, bw, w, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+        c.gemm(false, false, mp, w, bw, -1.0, Wu, m, Z2, bw, 1.0, dr, ld);
+        c.gemm(true, false, bw, w, bw, 1.0, Us, b, dr, ld, 0.0, Z1, bw);          // A12 := U_s^T A12
+        launch_copy(st, bw, w, Z1, bw, dr, ld);
+        if (next_sketch)
+          c.gemm(true, false, w, b, mp - b, 1.0, d + j0 + b, ld, G, mp - b, 0.0, Y + (col - j0 - b), np - b);
+      });
+      y_ready = next_sketch;
+    }
+  }
+}
+
+// z = T11^{-1} C(0:r) into the zsolve buffer, T's column blocks fetched bottom-up (rows 0:j1).
+void solve_z_ooc(const Ctx& c, Ooc& o, int64_t r, const double* Cd, int64_t ldc, int64_t k) {
+  cudaStream_t st = c.st;
+  if (r <= 0 || k <= 0) return;
+  double* Zb = c.at(c.L.zsolve);
+  double* D = c.at(c.L.R);
+  launch_copy(st, r, k, Cd, ldc, Zb, r);
+  const int64_t b = o.b;
+  for (int64_t j0 = ((r - 1) / b) * b; j0 >= 0; j0 -= b) {
+    const int64_t j1 = std::min(r, j0 + b), w = j1 - j0;
+    int64_t ldt = o.m;
+    const double* Tb = ooc_block(o, c, j0, w, j1, &ldt);
+    launch_copy(st, w, w, Tb + j0, ldt, D, b);
+    launch_trsv_block(st, 0, w, D, b, Zb + j0, r, k);
+    if (j0 > 0) c.gemm(false, false, j0, k, w, -1.0, Tb, ldt, Zb + j0, r, 1.0, Zb, r);
+  }
+}
+
 bool is_device_ptr(const void* p) {
   if (!p) return true;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// utv_lstsq with UTV_HOST_STREAMED: A (host, overwritten by T), B / X host or device.
+int64_t lstsq_streamed(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
+                       double* X, int64_t ldx, const utv_opts& opt) {
+  if (is_device_ptr(A)) fail(UTV_ERR_ARG, "UTV_HOST_STREAMED needs A in host memory");
+  if (opt.flags & (UTV_NULLIFY_T12 | UTV_EXPLICIT_V))
+    fail(UTV_ERR_UNSUPPORTED, "UTV_HOST_STREAMED is implemented for the fast option with factored V only");
+  cudaStream_t st = h->stream;
+  const int64_t b = opt.block;
+  // pin A for the DMA engines if the caller did not (unpinned for the duration of the call)
+  struct Pin {
+    void* p = nullptr;
+    ~Pin() { if (p) { cudaHostUnregister(p); cudaGetLastError(); } }
+  } pin;
+  if (!is_pinned_host_ptr(A)) {
+    UTV_CUDA(cudaHostRegister(A, ((size_t)(n - 1) * lda + m) * sizeof(double), cudaHostRegisterDefault));
+    pin.p = A;
+  }
+  if (!h->h2d) {
+    UTV_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+    UTV_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+    for (int s = 0; s < utv_handle_s::kStg; ++s) {
+      UTV_CUDA(cudaEventCreateWithFlags(&h->ev_loaded[s], cudaEventDisableTiming));
+      UTV_CUDA(cudaEventCreateWithFlags(&h->ev_free[s], cudaEventDisableTiming));
+    }
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_wb, cudaEventDisableTiming));
+  }
+  h->ooc_h2d = h->ooc_d2h = 0;
+  // fixed device memory: workspace, factored V, then the OOC arena (C, X, diag, panel, staging)
+  Ctx c = make_ctx(h, m, n, k, b);
+  const int64_t nsteps = (n + b - 1) / b;
+  const size_t wdbl = factored_w_doubles(n, b), tdbl = (size_t)nsteps * b * b;
+  ensure_buf(&h->vbuf, &h->vbuf_doubles, wdbl + 2 * tdbl + 64);
+  FactoredV fv;
+  fv.W = h->vbuf; fv.T = h->vbuf + wdbl; fv.Vs = fv.T + tdbl;
+  static const int64_t chunk_blocks = [] {
+    const char* e = std::getenv("UTV_OOC_CHUNK_BLOCKS");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : (int64_t)4;
+  }();
+  const int64_t cw = std::min<int64_t>(chunk_blocks * b, (n + b - 1) / b * b);
+  const size_t kk = (size_t)std::max<int64_t>(k, 1);
+  const size_t fixed = (size_t)m * kk + (size_t)n * kk + (size_t)n + 64 + (size_t)m * b +
+                       (size_t)utv_handle_s::kStg * m * cw;
+  size_t free_b = 0, total_b = 0;
+  UTV_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t used_b = (h->ws_doubles + h->vbuf_doubles + h->ooc_doubles) * sizeof(double);
+  size_t avail = free_b + h->ooc_doubles * sizeof(double);                 // the OOC arena is reused
+  avail = avail > ((size_t)1 << 30) ? avail - ((size_t)1 << 30) : 0;       // 1 GiB head room
+  if (h->dev_budget > 0) {
+    const size_t cap = (size_t)h->dev_budget > used_b - h->ooc_doubles * sizeof(double)
+                           ? (size_t)h->dev_budget - (used_b - h->ooc_doubles * sizeof(double)) : 0;
+    avail = std::min(avail, cap);
+  }
+  if (avail < fixed * sizeof(double))
+    fail(UTV_ERR_ALLOC, "device budget too small for the streamed working set (" +
+                            std::to_string(fixed * sizeof(double) + used_b) + " bytes needed)");
+  int64_t res_cols = (int64_t)((avail / sizeof(double) - fixed) / (size_t)m);
+  if (const char* e = std::getenv("UTV_OOC_MAX_RESIDENT_COLS"))              // tests / benchmarks
+    res_cols = std::min<int64_t>(res_cols, std::max<int64_t>(0, std::atoll(e)));
+  Ooc o;
+  o.h = h; o.m = m; o.n = n; o.b = b; o.hA = A; o.lda = lda; o.cw = cw;
+  o.c_res = res_cols >= n ? 0 : std::min<int64_t>(n, (n - res_cols + b - 1) / b * b);
+  const size_t total = fixed + (size_t)m * (n - o.c_res);
+  if (h->ooc_doubles < total) {
+    if (h->ooc) { UTV_CUDA(cudaFree(h->ooc)); h->ooc = nullptr; h->ooc_doubles = 0; }
+    ensure_buf(&h->ooc, &h->ooc_doubles, total);
+  }
+  double* p = h->ooc;
+  double* Cd = p; p += (size_t)m * kk;
+  double* Xd = p; p += (size_t)n * kk;
+  double* dg = p; p += (size_t)n + 64;
+  o.pb = p; p += (size_t)m * b;
+  for (int s = 0; s < utv_handle_s::kStg; ++s) { o.stg[s] = p; p += (size_t)m * cw; }
+  o.res = p;
+  h->ooc_resident_cols = n - o.c_res;
+  if (k > 0) copy2d(st, Cd, m, B, ldb, m, k, is_device_ptr(B) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+  factor_ooc(c, o, k > 0 ? Cd : nullptr, m, k, opt, &fv, dg);
+  const int64_t r = finish_factor(c, n, dg, 0, opt.tau, true);              // ldt = 0: T_jj = dg[j]
+  if (k > 0) {
+    solve_z_ooc(c, o, r, Cd, m, k);
+    solve_factored(c, n, r, nullptr, 0, nullptr, 0, k, Xd, n, fv, b, nullptr, true);
+  }
+  if (o.c_res < n) {                                                        // resident part of T
+    UTV_CUDA(cudaEventRecord(h->ev_done, st));
+    UTV_CUDA(cudaStreamWaitEvent(h->d2h, h->ev_done, 0));
+    copy2d(h->d2h, A + cm(0, o.c_res, lda), lda, o.res, m, m, n - o.c_res, cudaMemcpyDeviceToHost);
+    h->ooc_d2h += (n - o.c_res) * m * 8;
+  }
+  if (k > 0) {
+    if (is_device_ptr(B)) copy2d(st, B, ldb, Cd, m, m, k, cudaMemcpyDeviceToDevice);
+    copy2d(st, X, ldx, Xd, n, n, k, is_device_ptr(X) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+  }
+  UTV_CUDA(cudaStreamSynchronize(h->d2h));
+  UTV_CUDA(cudaStreamSynchronize(st));
+  return r;
 }
 
 }  // namespace
@@ -578,6 +903,15 @@ utv_status utv_destroy(utv_handle h) {
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->ev_panel) cudaEventDestroy(h->ev_panel);
   if (h->ev_svd) cudaEventDestroy(h->ev_svd);
+  if (h->h2d) { cudaStreamSynchronize(h->h2d); cudaStreamDestroy(h->h2d); }
+  if (h->d2h) { cudaStreamSynchronize(h->d2h); cudaStreamDestroy(h->d2h); }
+  for (int s = 0; s < utv_handle_s::kStg; ++s) {
+    if (h->ev_loaded[s]) cudaEventDestroy(h->ev_loaded[s]);
+    if (h->ev_free[s]) cudaEventDestroy(h->ev_free[s]);
+  }
+  if (h->ev_done) cudaEventDestroy(h->ev_done);
+  if (h->ev_wb) cudaEventDestroy(h->ev_wb);
+  cudaFree(h->ooc);
   cudaFree(h->bar2);
   cudaFree(h->ws); cudaFree(h->bar); cudaFree(h->info); cudaFree(h->flag); cudaFree(h->d_rank);
   cudaFree(h->vbuf); cudaFree(h->stage); cudaFree(h->nbuf);
@@ -642,6 +976,11 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
     if ((n > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
     if (n == 0) { if (rank) *rank = 0; return; }
+    if (opts->flags & UTV_HOST_STREAMED) {
+      const int64_t r = lstsq_streamed(h, m, n, k, A, lda, B, ldb, X, ldx, *opts);
+      if (rank) *rank = r;
+      return;
+    }
     cudaStream_t st = h->stream;
     // host buffers (the end-to-end path): stage through device memory on the stream
     const bool hA = !is_device_ptr(A), hB = k > 0 && !is_device_ptr(B), hX = k > 0 && !is_device_ptr(X);
@@ -816,6 +1155,21 @@ utv_status utv_rank(utv_handle h, int64_t n, const double* T, int64_t ldt, doubl
     UTV_CUDA(cudaMemcpyAsync(h->h_rank, h->d_rank, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
     UTV_CUDA(cudaStreamSynchronize(h->stream));
     *rank = *h->h_rank;
+  });
+}
+
+utv_status utv_set_device_budget(utv_handle h, int64_t bytes) {
+  return guarded(h, [&] {
+    if (bytes < 0) fail(UTV_ERR_ARG, "bytes < 0");
+    h->dev_budget = bytes;
+  });
+}
+
+utv_status utv_stream_stats(utv_handle h, int64_t* h2d_bytes, int64_t* d2h_bytes, int64_t* resident_cols) {
+  return guarded(h, [&] {
+    if (h2d_bytes) *h2d_bytes = h->ooc_h2d;
+    if (d2h_bytes) *d2h_bytes = h->ooc_d2h;
+    if (resident_cols) *resident_cols = h->ooc_resident_cols;
   });
 }
 

@@ -1,0 +1,125 @@
+"""Out-of-core randUTV least squares (UTV_HOST_STREAMED) against the CPU oracle.
+
+A stays in host memory and is streamed through HBM in column chunks; the device keeps only as
+many trailing column blocks as the budget (here capped with UTV_OOC_MAX_RESIDENT_COLS) allows.
+Gates as for the in-core path: r identical, x within 1e-9 of the oracle;
+the T left in host memory has the oracle's diagonal (the singular values of every diagonal
+block, which do not depend on the SVD signs, R20) and an exactly zero strictly-lower part (R13).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import utv_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def utv():
+    from paper_2408_05238_b200 import build
+    build.build()
+    import paper_2408_05238_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def h(utv):
+    hd = utv.Handle(0)
+    yield hd
+    hd.close()
+
+
+def host_colmajor(a, pin):
+    a = np.asarray(a, dtype=np.float64)
+    t = torch.from_numpy(np.ascontiguousarray(a.T)).t()
+    return t.pin_memory() if pin else t.clone()
+
+
+def streamed(utv, h, A, B, b, q, seed, pin=True, device_b=False, k=None):
+    m, n = A.shape
+    At = host_colmajor(A, pin)
+    Bt = host_colmajor(B.reshape(m, -1), pin)
+    if device_b:
+        Bt = Bt.cuda()
+    kk = Bt.shape[1]
+    X = utv.colmajor_empty(n, kk, device="cpu", pin_memory=pin)
+    r = h.lstsq(At, Bt, X, utv.Opts(block=b, power_iters=q, tau=1e-10, seed=seed, flags=utv.UTV_HOST_STREAMED))
+    return At.numpy(), Bt, X.numpy(), r
+
+
+@pytest.mark.parametrize("m,n,r,b,q,k,cap,pin", [
+    (600, 600, 300, 64, 1, 2, 0, True),         # every block streamed
+    (700, 550, 260, 64, 2, 3, 192, True),       # ragged last block, 3 blocks resident
+    (640, 512, 200, 64, 1, 1, 10**9, False),    # everything resident; pageable A (registered)
+    (900, 640, 333, 128, 2, 2, 128, True),      # b = 128, r inside a block
+])
+def test_streamed_lstsq_matches_oracle(utv, h, monkeypatch, m, n, r, b, q, k, cap, pin):
+    monkeypatch.setenv("UTV_OOC_MAX_RESIDENT_COLS", str(cap))
+    M = gen.GpMatrix(m, n, r, seed=m + n + b)
+    B, X0 = M.known_rhs(k=k)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=5)
+    T, _, Xg, rg = streamed(utv, h, M.A, B, b, q, 5, pin=pin)
+    st = h.stream_stats()
+    assert rg == ro == r
+    assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
+    assert np.linalg.norm(Xg - X0) <= 1e-10 * np.linalg.norm(X0)
+    # T in host memory: oracle's diagonal, strictly-lower part exactly zero
+    To = oracle.randutv(M.A, b, q, 5)["T"]
+    d, do = np.diag(T), np.diag(To)
+    assert np.all(d >= 0.0)
+    assert np.max(np.abs(d - do)) <= 1e-12 * np.max(do)
+    assert np.all(np.tril(T, -1) == 0.0)
+    # traffic: resident columns as capped, streamed columns moved both ways
+    assert st["resident_cols"] == (n if cap >= n else n - min(n, (n - cap + b - 1) // b * b))
+    if cap < n:
+        assert st["h2d_bytes"] > 8 * m * n and st["d2h_bytes"] >= 8 * m * (n - st["resident_cols"])
+
+
+def test_streamed_equals_in_core(utv, h, monkeypatch):
+    """Same seeded problem through both paths: identical rank, x to 1e-12 (rounding only)."""
+    monkeypatch.setenv("UTV_OOC_MAX_RESIDENT_COLS", "512")
+    m, n, r, b, q = 2048, 2048, 1000, 256, 2
+    M = gen.GpMatrix(m, n, r, seed=41)
+    B, X0 = M.known_rhs(k=1)
+    T, _, Xs, rs = streamed(utv, h, M.A, B, b, q, 7)
+    Ad = torch.from_numpy(np.ascontiguousarray(M.A.T)).cuda().t()
+    Bd = torch.from_numpy(np.ascontiguousarray(B.reshape(m, 1).T)).cuda().t()
+    Xd, rd = utv.lstsq(Ad, Bd, utv.Opts(block=b, power_iters=q, tau=1e-10, seed=7), handle=h)
+    Xd = Xd.cpu().numpy()
+    assert rs == rd == r
+    assert np.linalg.norm(Xs - Xd) <= 1e-12 * np.linalg.norm(Xd)
+    assert np.linalg.norm(Xs - X0) <= 1e-10 * np.linalg.norm(X0)
+
+
+def test_streamed_device_b_becomes_utb(utv, h, monkeypatch):
+    """A device B is overwritten by C = U^T B: ||A x - b|| == ||C[r:m]|| (P11)."""
+    monkeypatch.setenv("UTV_OOC_MAX_RESIDENT_COLS", "64")
+    m, n, r, b = 500, 400, 150, 64
+    M = gen.GpMatrix(m, n, r, seed=3)
+    B, _ = M.known_rhs(k=2)
+    _, Cd, Xg, rg = streamed(utv, h, M.A, B, b, 1, 2, device_b=True)
+    Cm = Cd.cpu().numpy()
+    res = np.linalg.norm(M.A @ Xg - B.reshape(m, -1))
+    assert rg == r
+    assert abs(res - np.linalg.norm(Cm[r:])) <= 1e-12 * np.linalg.norm(B)
+
+
+def test_streamed_errors(utv, h):
+    A = utv.colmajor_empty(64, 64).zero_()
+    B = utv.colmajor_empty(64, 1).zero_()
+    X = utv.colmajor_empty(64, 1).zero_()
+    with pytest.raises(utv.UtvError) as e:                  # A must be in host memory
+        h.lstsq(A, B, X, utv.Opts(block=16, flags=utv.UTV_HOST_STREAMED))
+    assert e.value.status == utv.UTV_ERR_ARG
+    Ah = utv.colmajor_empty(64, 64, device="cpu")
+    Ah.zero_()
+    with pytest.raises(utv.UtvError) as e:
+        h.lstsq(Ah, B, X, utv.Opts(block=16, flags=utv.UTV_HOST_STREAMED | utv.UTV_NULLIFY_T12))
+    assert e.value.status == utv.UTV_ERR_UNSUPPORTED
+    h.set_device_budget(1 << 20)                             # 1 MiB cannot hold the workspace
+    with pytest.raises(utv.UtvError) as e:
+        h.lstsq(Ah, B, X, utv.Opts(block=16, flags=utv.UTV_HOST_STREAMED))
+    assert e.value.status == utv.UTV_ERR_ALLOC
+    h.set_device_budget(0)
