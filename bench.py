@@ -84,6 +84,18 @@ def fp64_peak():
         return 37.2, "fallback: DMMA microbenchmark value of round 1"
 
 
+def gemm_traffic():
+    """DRAM traffic per launch of the dominant GEMM launch of the step (cfg3 step-0 sketch product),
+    from the committed ncu --set full capture (profiles/r01_gemm_traffic.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")))
+        l0 = d["launches"][0]
+        return {"traffic": l0["traffic_bytes"], "traffic_algorithmic": l0["algorithmic_bytes"],
+                "traffic_launch": l0["shape"] + "; " + d["source"]}
+    except Exception:
+        return {"traffic": None}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -355,7 +367,7 @@ def run_ours(args):
         "fp64_peak_tflops": peak, "f_alg": F, "rank": r, "rank_ok": r == r_true, "rel_err_x0": rel_err,
         "roofline": {"kernel": "dgemm_tma_kernel (TMA-fed FP64 mma.sync DMMA; all GEMM launches of the step)",
                      "bound": "tensor", "achieved": gemm_tf, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (gemm_tf / peak) if gemm_tf else None, "traffic": None,
+                     "frac": (gemm_tf / peak) if gemm_tf else None, **gemm_traffic(),
                      "peak_source": peak_src,
                      "share_of_step": g["ms"] / (t * 1e3 * args.steps) if t > 0 else None},
         "phases_ms_per_step": {k2: v["ms"] / args.steps for k2, v in prof.items()},
@@ -372,6 +384,70 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_streamed(args):
+    """Out-of-core mode (UTV_HOST_STREAMED): A in pinned host memory, at most
+    --streamed columns resident in HBM, the rest streamed every pass.  Bound: the host link."""
+    import torch
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda:0")
+    import paper_2408_05238_b200 as utv
+    import utv_inputs as gen
+    m, n, r_true, b, q, k = CONFIGS[args.config]
+    opts = utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED, flags=utv.UTV_HOST_STREAMED)
+    os.environ["UTV_OOC_MAX_RESIDENT_COLS"] = str(args.streamed)
+    At, Bm, X0 = gen.gp_torch(m, n, r_true, seed=gen.MATRIX_SEED, device=dev, k=k)
+    A0 = At.t().cpu()
+    B0 = utv.colmajor(Bm).cpu()
+    X0 = X0.cpu()
+    del At, Bm
+    torch.cuda.empty_cache()
+    h = utv.Handle(0)
+    Ah = utv.colmajor_empty(m, n, device="cpu", pin_memory=True)
+    Bh = utv.colmajor_empty(m, k, device="cpu", pin_memory=True)
+    Xh = utv.colmajor_empty(n, k, device="cpu", pin_memory=True)
+    times, r = [], -1
+    clocks = ClockSampler(0)
+    for it in range(args.warmup + args.steps):
+        Ah.copy_(A0); Bh.copy_(B0)
+        if it == args.warmup:
+            clocks.start()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = h.lstsq(Ah, Bh, Xh, opts)             # synchronises at the end (host X)
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    clk = clocks.stop()
+    st = h.stream_stats()
+    t = statistics.median(times)
+    F = f_alg(m, n, b, q, k, r)
+    link = (st["h2d_bytes"] + st["d2h_bytes"]) / t / 1e9
+    peaks = json.load(open(FP64_PEAK_FILE))
+    link_peak = peaks["h2d_pinned_gbs"] + peaks["d2h_pinned_gbs"]
+    out = {
+        "metric": METRIC, "value": F / t / 1e12, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "time_to_solution_s": t, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "ours-streamed",
+        "config": {"workload": f"{args.config} out-of-core (UTV_HOST_STREAMED): A in pinned host memory, "
+                               f"<= {args.streamed} columns resident in HBM", "m": m, "n": n, "rank": r_true,
+                   "block": b, "power_iters": q, "rhs": k, "parallelism": "single",
+                   "step": "copy A,B into pinned host buffers (untimed) + utv_lstsq(host A, B, X)"},
+        "rank": r, "rank_ok": r == r_true, "rel_err_x0": float(((Xh - X0).norm() / X0.norm()).item()),
+        "stream": st,
+        "roofline": {"kernel": "host<->device column-chunk streaming (cudaMemcpy2DAsync on two copy streams)",
+                     "bound": "host-link", "achieved": link, "peak": link_peak, "unit": "GB/s",
+                     "frac": link / link_peak, "traffic": st["h2d_bytes"] + st["d2h_bytes"],
+                     "peak_source": "profiles/r01_fp64_peaks.json: pinned H2D + D2H copy bandwidth (full duplex)"},
+        "e2e": {"value": F / t / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": st["h2d_bytes"],
+                "d2h_bytes_per_step": st["d2h_bytes"]},
+        "clocks": clk,
+    }
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -385,8 +461,12 @@ def main():
     ap.add_argument("--ref-n", type=int, default=1536)
     ap.add_argument("--force-dist", action="store_true", help="use the multi-GPU (block-cyclic) path even at N=1")
     ap.add_argument("--profile-dump", default="", help="write every timed launch record as CSV (diagnostics)")
+    ap.add_argument("--streamed", type=int, default=-1,
+                    help="out-of-core mode: keep at most this many columns of A resident in HBM")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.streamed >= 0:
+        run_streamed(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
