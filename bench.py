@@ -11,7 +11,7 @@ for the whole job.  Inputs (20 GB) are far larger than the 126 MB L2, so no flus
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
 
 N > 1 (torchrun): ONE cfg3 problem on all ranks (strong scaling): block-cyclic columns, NCCL
-AllReduce / AllGather / Broadcast per step (paper_2408_05238_b200.dist).
+AllReduce / AllGather / Broadcast per step inside libutv.so (utv_create_dist).
 `--impl reference`: the CPU oracle (oracle/, the only comparison program that exists for this
 paper) timed on the host cores on a bounded sample of the same recipe.
 """
@@ -221,20 +221,28 @@ def run_ours(args):
     stream = h.stream
     use_dist = world > 1 or args.force_dist
     if use_dist:
-        # strong scaling: the block-cyclic multi-GPU path solves ONE problem
+        # strong scaling: the native block-cyclic multi-GPU path (utv_create_dist,
+        # NCCL communicator of libutv.so) solves ONE problem on all ranks
         from paper_2408_05238_b200 import dist as D
         A0 = D.scatter_columns(A0, b, world, rank)   # this rank's pristine shard
         del At
         torch.cuda.empty_cache()
-        A = utv.colmajor_empty(m, A0.shape[1], device=dev)
-        steps_backend = D.CudaSteps(h)
-        Xbox = [None]
+        uid = [utv.get_unique_id() if rank == 0 else None]
+        if world > 1:
+            torch.distributed.broadcast_object_list(uid, src=0)
+        h.close()
+        h = utv.dist_handle(uid[0], world, rank, device=dev.index)
+        stream = h.stream
+        A = utv.colmajor_empty(m, max(1, A0.shape[1]), device=dev)
+        B = utv.colmajor_empty(m, k, device=dev)
+        Xs = utv.colmajor_empty(n, k, device=dev)
+        Xbox = [Xs]
 
         def step():
-            A.copy_(A0)
-            Xd, rr = D.lstsq_dist(A, B0, n, b=b, q=q, tau=opts.tau, seed=opts.seed, steps=steps_backend)
-            Xbox[0] = Xd
-            return rr
+            if A0.shape[1]:
+                A[:, :A0.shape[1]].copy_(A0)
+            B.copy_(B0)
+            return h.lstsq(A, B, Xs, opts)
     else:
         A = utv.colmajor_empty(m, n, device=dev)
         B = utv.colmajor_empty(m, k, device=dev)
@@ -280,9 +288,9 @@ def run_ours(args):
     F = f_alg(m, n, b, q, k, r)
     # value: F_alg is SURVEY 8(d)'s fixed, implementation-independent workload measure (App. B,
     # V counted as accumulated explicitly), so F_alg / t is an inverse time-to-solution.  The
-    # hardware rate uses the flops this implementation executes: the single-GPU path keeps V
-    # factored (no explicit accumulation), the multi-GPU path accumulates V explicitly.
-    factored = not use_dist
+    # hardware rate uses the flops this implementation executes: V is kept factored (no explicit
+    # accumulation) on one GPU and, replicated, on the multi-GPU path.
+    factored = True                               # both paths keep V factored
     F_exec = F - v_accum_flops(m, n, b) + factored_apply_flops(n, b, k, r) if factored else F
     value = F / t / 1e12                          # one problem on all ranks (strong scaling)
     executed_tflops = F_exec / t / 1e12
@@ -299,10 +307,12 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        Xd = utv.colmajor_empty(n, k, device=dev)
         e0.record(stream)
-        A.copy_(Ah, non_blocking=True)
+        if A0.shape[1]:
+            A[:, :A0.shape[1]].copy_(Ah, non_blocking=True)
         Bd.copy_(Bh, non_blocking=True)
-        Xd, re = D.lstsq_dist(A, Bd, n, b=b, q=q, tau=opts.tau, seed=opts.seed, steps=steps_backend)
+        re = h.lstsq(A, Bd, Xd, opts)
         Xh = Xd.cpu()
         e1.record(stream)
         torch.cuda.synchronize()
@@ -356,8 +366,8 @@ def run_ours(args):
                    "power_iters": q, "rhs": k,
                    "parallelism": f"blockcyclic{world}" if use_dist else "single",
                    "l2": "inputs (8mn = %.1f GB) >> 126 MB L2; no flush needed" % (8 * m * n / 1e9),
-                   "step": ("restore the rank's A shard from a pristine device copy (D2D) + lstsq_dist "
-                            "(block-cyclic columns, NCCL)") if use_dist else
+                   "step": ("restore the rank's A shard from a pristine device copy (D2D) + utv_lstsq on a "
+                            "utv_create_dist handle (block-cyclic columns, NCCL)") if use_dist else
                            "restore A,B from a pristine device copy (D2D) + utv_lstsq"},
         "value_definition": "F_alg (SURVEY App. B, fixed workload incl. explicit-V accumulation) / "
                             "time-to-solution; executed_tflops counts the flops actually executed",

@@ -61,10 +61,35 @@ typedef struct {
  * legacy default stream).  Returns UTV_ERR_CUDA if the device is unusable. */
 utv_status utv_create(utv_handle* handle, int device, void* stream);
 
-/* Multi-GPU handle (block-cyclic columns over NCCL).  Not provided by this
- * build: returns UTV_ERR_UNSUPPORTED. */
+/*
+ * Multi-GPU handles: one rank per GPU, 1D block-cyclic columns (block n_b = opts->block,
+ * block j on rank j mod P).  With such a handle utv_lstsq takes A = THIS RANK's shard: its column
+ * blocks packed in order (m x utv_dist_local_cols(n, n_b, P, rank), lda >= m, device memory) and
+ * n = the GLOBAL column count; B (m x k, device) is replicated on every rank and overwritten by
+ * U^T B; X (n x k, device) is written, identical on every rank; *rank is identical on every rank.
+ * All ranks must make the same calls with the same m, n, k, opts (collectives in lock step).
+ * Fast option with factored V only (UTV_NULLIFY_T12 / UTV_EXPLICIT_V / UTV_HOST_STREAMED ->
+ * UTV_ERR_UNSUPPORTED); utv_factor on such a handle -> UTV_ERR_UNSUPPORTED.  A communication
+ * failure returns UTV_ERR_NCCL.
+ */
+/* NCCL unique id (128 bytes) for utv_create_dist; call on one rank and share it (e.g. through
+ * torch.distributed).  libnccl.so.2 is loaded at run time; UTV_ERR_NCCL if it is unavailable. */
+utv_status utv_get_unique_id(void* nccl_uid);
+
+/* One process per GPU: rank `rank` of `nranks`, NCCL communicator from nccl_uid (ncclCommInitRank
+ * on `device`; collective with the other ranks). */
 utv_status utv_create_dist(utv_handle* handle, int device, void* stream, const void* nccl_uid,
                            int nranks, int rank);
+
+/* One process, several ranks (one host thread per handle): handles[r] is rank r of an in-process
+ * group on devices[r] with streams[r] (NULL = legacy default streams).  Collectives rendezvous on
+ * the host and combine the peers' device buffers in rank order; each handle must be driven by its
+ * own thread.  Destroy each handle with utv_destroy. */
+utv_status utv_create_local_group(utv_handle* handles, int nranks, const int* devices,
+                                  void* const* streams);
+
+/* Number of columns of rank `rank`'s shard of an n-column matrix (block-cyclic, block `block`). */
+int64_t utv_dist_local_cols(int64_t n, int64_t block, int nranks, int rank);
 
 /* Release the handle and its workspace (synchronises its stream).  NULL is accepted. */
 utv_status utv_destroy(utv_handle handle);

@@ -27,7 +27,8 @@ EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "u
             "utv_factor", "utv_solve", "utv_lstsq", "utv_version", "utv_sketch", "utv_philox", "utv_hqr",
             "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read",
             "utv_profile_dump", "utv_svd_block", "utv_svd_status", "utv_trsm_upper",
-            "utv_rank_diag", "utv_set_device_budget", "utv_stream_stats"]
+            "utv_rank_diag", "utv_set_device_budget", "utv_stream_stats", "utv_get_unique_id",
+            "utv_create_local_group", "utv_dist_local_cols"]
 PROF_FAMILIES = ["gemm", "panel", "svd", "sketch", "solve", "misc"]
 
 
@@ -97,6 +98,9 @@ def lib() -> C.CDLL:
             "utv_trsm_upper": ([p, i64, p, i64, p, i64, i64], st),
             "utv_rank_diag": ([p, i64, p, d, C.POINTER(i64)], st),
             "utv_set_device_budget": ([p, i64], st),
+            "utv_get_unique_id": ([p], st),
+            "utv_create_local_group": ([p, C.c_int, p, p], st),
+            "utv_dist_local_cols": ([i64, i64, C.c_int, C.c_int], i64),
             "utv_stream_stats": ([p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], st),
         }
         for name, (args, res) in sig.items():
@@ -157,6 +161,13 @@ class Handle:
         self._check(lib().utv_create(C.byref(h), self.device, C.c_void_p(self.stream.cuda_stream)), None)
         self.h = h
 
+    @classmethod
+    def _wrap(cls, h: C.c_void_p, device: int, stream) -> "Handle":
+        obj = cls.__new__(cls)
+        obj.device, obj.stream, obj.h = device, stream, h
+        obj.multi = True
+        return obj
+
     def _check(self, status: int, h):
         if status != UTV_OK:
             msg = lib().utv_last_error(h).decode() if h is not None else "utv_create failed"
@@ -208,10 +219,13 @@ class Handle:
         return X
 
     def lstsq(self, A, B, X, opts: Opts | None = None) -> int:
-        """Fast-option LS (A, B consumed).  A, B, X may be device or host tensors."""
+        """Fast-option LS (A, B consumed).  A, B, X may be device or host tensors.  On a multi-GPU
+        handle A is this rank's block-cyclic shard and the global n is X.shape[0]."""
         opts = opts or Opts()
         _check_f64(A, B, X)
         m, n = A.shape
+        if getattr(self, "multi", False):
+            n = X.shape[0]
         k = B.shape[1] if B.dim() == 2 else 1
         r = C.c_int64(-1)
         o = opts.c()
@@ -340,3 +354,43 @@ def lstsq(A, B, opts: Opts | None = None, handle: Handle | None = None):
     X = colmajor_empty(n, k, device=A.device) if A.is_cuda else colmajor_empty(n, k, device="cpu")
     r = h.lstsq(A, B if B.dim() == 2 else B.reshape(-1, 1), X, opts)
     return X, r
+
+
+# ----------------------------------------------------------------------------- multi-GPU handles
+def get_unique_id() -> bytes:
+    """NCCL unique id (128 bytes) for dist_handle(); create it on one rank and share it."""
+    buf = C.create_string_buffer(128)
+    st = lib().utv_get_unique_id(buf)
+    if st != UTV_OK:
+        raise UtvError(st, "utv_get_unique_id failed (libnccl.so.2 unavailable?)")
+    return buf.raw
+
+
+def dist_handle(nccl_uid: bytes, nranks: int, rank: int, device: int | None = None) -> Handle:
+    """Rank `rank` of an NCCL multi-GPU handle (one process per GPU; utv_create_dist)."""
+    device = torch.cuda.current_device() if device is None else int(device)
+    stream = torch.cuda.current_stream(device)
+    h = C.c_void_p()
+    uid = C.create_string_buffer(bytes(nccl_uid), 128)
+    st = lib().utv_create_dist(C.byref(h), device, C.c_void_p(stream.cuda_stream), uid, nranks, rank)
+    if st != UTV_OK:
+        raise UtvError(st, "utv_create_dist failed")
+    return Handle._wrap(h, device, stream)
+
+
+def local_group(nranks: int, devices=None, streams=None) -> list:
+    """nranks handles forming one in-process multi-GPU group (utv_create_local_group); drive each
+    handle from its own thread.  devices default to the current device for every rank."""
+    devices = [torch.cuda.current_device()] * nranks if devices is None else list(devices)
+    streams = [torch.cuda.Stream(device=d) for d in devices] if streams is None else list(streams)
+    hs = (C.c_void_p * nranks)()
+    devs = (C.c_int * nranks)(*devices)
+    sts = (C.c_void_p * nranks)(*[s.cuda_stream for s in streams])
+    st = lib().utv_create_local_group(hs, nranks, devs, sts)
+    if st != UTV_OK:
+        raise UtvError(st, "utv_create_local_group failed")
+    return [Handle._wrap(C.c_void_p(hs[r]), devices[r], streams[r]) for r in range(nranks)]
+
+
+def dist_local_cols(n: int, block: int, nranks: int, rank: int) -> int:
+    return int(lib().utv_dist_local_cols(n, block, nranks, rank))

@@ -60,6 +60,12 @@ void launch_set_zero(cudaStream_t st, int64_t rows, int64_t cols, double* A, int
 void launch_set_diag(cudaStream_t st, int64_t bw, const double* sigma, double* A, int64_t lda);
 void launch_copy(cudaStream_t st, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd);
 void launch_zero_strict_lower(cudaStream_t st, int64_t rows, int64_t cols, double* A, int64_t lda);
+void launch_axpy(cudaStream_t st, int64_t n, double alpha, const double* x, double* y);   // y += alpha x (contiguous)
+// multi-GPU block-cyclic helpers (misc.cu): see the kernels' comments
+void launch_assemble_y(cudaStream_t st, int64_t np, int64_t cols, int64_t b, int64_t i, int P, int64_t Lmax,
+                       const double* recv, double* Y, int64_t ldy);
+void launch_gather_local(cudaStream_t st, int64_t nloc, int64_t cols, int64_t b, int64_t i, int P, int p,
+                         const double* W, int64_t ldw, double* D, int64_t ldd);
 // flag[0] |= any non-finite entry in A (rows x cols)
 void launch_check_finite(cudaStream_t st, int64_t rows, int64_t cols, const double* A, int64_t lda, int* flag);
 

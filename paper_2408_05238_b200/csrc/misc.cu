@@ -72,6 +72,58 @@ void launch_set_diag(cudaStream_t st, int64_t bw, const double* sigma, double* A
   set_diag_kernel<<<grid_for(bw * bw), 256, 0, st>>>(bw, sigma, A, lda);
   UTV_CUDA(cudaGetLastError());
 }
+__global__ void axpy_kernel(int64_t n, double alpha, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    y[e] += alpha * x[e];
+}
+// Multi-GPU layout helpers (block-cyclic columns, block b, owner(blk) = blk mod P).
+// assemble_y: Y (np x cols, ldy) in global block order from the all-gathered per-rank row blocks
+// (rank o's trailing blocks, packed, at recv + o*Lmax*cols with ld Lmax): global block u = blk - i
+// comes from rank (i+u) mod P, where it is trailing block number u / P.
+__global__ void assemble_y_kernel(int64_t np, int64_t cols, int64_t b, int64_t i, int P, int64_t Lmax,
+                                  const double* __restrict__ recv, double* __restrict__ Y, int64_t ldy) {
+  const int64_t total = np * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e % np, c = e / np;
+    const int64_t u = row / b, rr = row % b;
+    const int64_t o = (i + u) % P, t = u / P;
+    Y[cm(row, c, ldy)] = recv[o * Lmax * cols + cm(t * b + rr, c, Lmax)];
+  }
+}
+// gather_local: the rows of W (np x cols, global trailing order from block i) that belong to rank p's
+// trailing blocks, packed: local trailing block t is global block u = ((p - i) mod P) + t P.
+__global__ void gather_local_kernel(int64_t nloc, int64_t cols, int64_t b, int64_t i, int P, int p,
+                                    const double* __restrict__ W, int64_t ldw, double* __restrict__ D, int64_t ldd) {
+  const int64_t total = nloc * cols;
+  const int64_t u0 = (((int64_t)p - i) % P + P) % P;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e % nloc, c = e / nloc;
+    const int64_t t = row / b, rr = row % b;
+    D[cm(row, c, ldd)] = W[cm((u0 + t * P) * b + rr, c, ldw)];
+  }
+}
+
+void launch_axpy(cudaStream_t st, int64_t n, double alpha, const double* x, double* y) {
+  if (n <= 0) return;
+  ProfScope prof(st, kProfMisc, 1, 2.0 * (double)n, 24.0 * (double)n);
+  axpy_kernel<<<grid_for(n), 256, 0, st>>>(n, alpha, x, y);
+  UTV_CUDA(cudaGetLastError());
+}
+void launch_assemble_y(cudaStream_t st, int64_t np, int64_t cols, int64_t b, int64_t i, int P, int64_t Lmax,
+                       const double* recv, double* Y, int64_t ldy) {
+  if (np * cols <= 0) return;
+  ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)(np * cols));
+  assemble_y_kernel<<<grid_for(np * cols), 256, 0, st>>>(np, cols, b, i, P, Lmax, recv, Y, ldy);
+  UTV_CUDA(cudaGetLastError());
+}
+void launch_gather_local(cudaStream_t st, int64_t nloc, int64_t cols, int64_t b, int64_t i, int P, int p,
+                         const double* W, int64_t ldw, double* D, int64_t ldd) {
+  if (nloc * cols <= 0) return;
+  ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)(nloc * cols));
+  gather_local_kernel<<<grid_for(nloc * cols), 256, 0, st>>>(nloc, cols, b, i, P, p, W, ldw, D, ldd);
+  UTV_CUDA(cudaGetLastError());
+}
+
 void launch_copy(cudaStream_t st, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd) {
   if (rows * cols <= 0) return;
   ProfScope prof(st, kProfMisc, 1, 0.0, 8.0 * (double)(rows * cols));

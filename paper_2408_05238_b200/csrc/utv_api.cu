@@ -1,8 +1,13 @@
 // utv_api.cu -- the C ABI of libutv.so (include/utv.h, include/utv_steps.h) and the host
 // orchestration of randUTV on one B200: the per-step launch sequence of fig:alg_utv
 // over the sm_100a kernels, the handle's workspace arena and error mapping.
+#include <dlfcn.h>
+#include <nccl.h>             // types and constants only; the functions are resolved with dlsym
+
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -14,6 +19,151 @@
 #include "prof.cuh"
 
 using namespace utv;
+
+// ------------------------------------------------------------------------------------------
+// Communicators of the multi-GPU path: NCCL (one process per GPU, utv_create_dist)
+// or an in-process group of ranks driven by host threads (utv_create_local_group).  In-place
+// sum-AllReduce, Broadcast and AllGather of FP64 device buffers, enqueued on the caller's stream.
+// ------------------------------------------------------------------------------------------
+struct Comm {
+  int nranks = 1, rank = 0;
+  virtual ~Comm() {}
+  virtual void allreduce(double* buf, size_t n, cudaStream_t st) = 0;
+  virtual void bcast(double* buf, size_t n, int root, cudaStream_t st) = 0;
+  virtual void allgather(const double* send, double* recv, size_t n, cudaStream_t st) = 0;
+};
+
+struct CommError {
+  std::string msg;
+};
+
+// NCCL, resolved at run time (libnccl.so.2 -- the one torch already loaded, if any), so that
+// libutv.so has no link-time NCCL dependency.
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* l = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!l) l = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!l) return;
+    NcclApi a;
+    a.lib = l;
+    a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(l, "ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(l, "ncclCommInitRank"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(l, "ncclCommDestroy"));
+    a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(l, "ncclAllReduce"));
+    a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(l, "ncclBroadcast"));
+    a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(l, "ncclAllGather"));
+    a.errorString = reinterpret_cast<decltype(a.errorString)>(dlsym(l, "ncclGetErrorString"));
+    if (a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.broadcast && a.allGather && a.errorString)
+      api = a;
+  });
+  return api.lib ? &api : nullptr;
+}
+
+struct NcclComm : Comm {
+  const NcclApi* api = nullptr;
+  ncclComm_t comm = nullptr;
+  void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw CommError{std::string(what) + ": " + api->errorString(r)};
+  }
+  void allreduce(double* buf, size_t n, cudaStream_t st) override {
+    if (n) check(api->allReduce(buf, buf, n, ncclFloat64, ncclSum, comm, st), "ncclAllReduce");
+  }
+  void bcast(double* buf, size_t n, int root, cudaStream_t st) override {
+    if (n) check(api->broadcast(buf, buf, n, ncclFloat64, root, comm, st), "ncclBroadcast");
+  }
+  void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
+    if (n) check(api->allGather(send, recv, n, ncclFloat64, comm, st), "ncclAllGather");
+  }
+  ~NcclComm() override {
+    if (comm && api) api->commDestroy(comm);
+  }
+};
+
+// In-process group: every rank is a host thread with its own handle and stream.  Collectives
+// rendezvous on the host (each rank first drains its stream), then every rank combines the peers'
+// device buffers in rank order (deterministic, identical on all ranks) with peer copies / adds.
+struct LocalGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const double*> ptr;
+  explicit LocalGroup(int n_) : n(n_), ptr(n_, nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LocalComm : Comm {
+  std::shared_ptr<LocalGroup> g;
+  double* tmp = nullptr;
+  size_t tmp_n = 0;
+  void ensure_tmp(size_t n) {
+    if (tmp_n >= n) return;
+    if (tmp) cudaFree(tmp);
+    tmp = nullptr; tmp_n = 0;
+    UTV_CUDA(cudaMalloc((void**)&tmp, n * sizeof(double)));
+    tmp_n = n;
+  }
+  void allreduce(double* buf, size_t n, cudaStream_t st) override {
+    if (!n) return;
+    ensure_tmp(n);
+    UTV_CUDA(cudaStreamSynchronize(st));
+    g->ptr[rank] = buf;
+    g->barrier();
+    UTV_CUDA(cudaMemcpyAsync(tmp, g->ptr[0], n * sizeof(double), cudaMemcpyDefault, st));
+    for (int r = 1; r < nranks; ++r) launch_axpy(st, (int64_t)n, 1.0, g->ptr[r], tmp);
+    UTV_CUDA(cudaStreamSynchronize(st));
+    g->barrier();                                            // every rank has read every buffer
+    UTV_CUDA(cudaMemcpyAsync(buf, tmp, n * sizeof(double), cudaMemcpyDefault, st));
+  }
+  void bcast(double* buf, size_t n, int root, cudaStream_t st) override {
+    if (!n) return;
+    UTV_CUDA(cudaStreamSynchronize(st));
+    g->ptr[rank] = buf;
+    g->barrier();
+    if (rank != root) {
+      UTV_CUDA(cudaMemcpyAsync(buf, g->ptr[root], n * sizeof(double), cudaMemcpyDefault, st));
+      UTV_CUDA(cudaStreamSynchronize(st));
+    }
+    g->barrier();
+  }
+  void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
+    if (!n) return;
+    UTV_CUDA(cudaStreamSynchronize(st));
+    g->ptr[rank] = send;
+    g->barrier();
+    for (int r = 0; r < nranks; ++r)
+      UTV_CUDA(cudaMemcpyAsync(recv + (size_t)r * n, g->ptr[r], n * sizeof(double), cudaMemcpyDefault, st));
+    UTV_CUDA(cudaStreamSynchronize(st));
+    g->barrier();
+  }
+  ~LocalComm() override {
+    if (tmp) cudaFree(tmp);
+  }
+};
 
 struct utv_handle_s {
   int device = 0;
@@ -43,6 +193,10 @@ struct utv_handle_s {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   static constexpr int kStg = 3;
   cudaEvent_t ev_loaded[kStg] = {}, ev_free[kStg] = {}, ev_done = nullptr, ev_wb = nullptr;
+  // multi-GPU (utv_create_dist / utv_create_local_group)
+  Comm* comm = nullptr;
+  int coop_share = 1;            // ranks of an in-process group sharing this device (cooperative-CTA cap)
+  double* dbuf = nullptr; size_t dbuf_doubles = 0;
   Profiler prof;
 };
 
@@ -77,6 +231,9 @@ utv_status guarded(utv_handle h, F&& f) {
                     std::to_string(e.line) + ")";
     cudaGetLastError();
     return e.err == cudaErrorMemoryAllocation ? UTV_ERR_ALLOC : UTV_ERR_CUDA;
+  } catch (const CommError& e) {
+    h->last_error = e.msg;
+    return UTV_ERR_NCCL;
   } catch (const std::bad_alloc&) {
     h->last_error = "host allocation failed";
     return UTV_ERR_ALLOC;
@@ -198,10 +355,12 @@ Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
   const Layout& L = c.L;
   c.side = h->side;
   // the main-stream panel kernels leave 16 SMs free for the concurrent side-stream Jacobi
+  // Cooperative (grid-barrier) panel kernels: ranks of an in-process group that share a device split
+  // its SMs, so that all their grids stay co-resident even when launched at the same time.
   c.pw = PanelWork{c.at(L.part), c.at(L.pz1), c.at(L.pz2), c.at(L.gram), c.at(L.px), c.at(L.gemm), L.gemm_doubles,
-                   h->bar, std::max(1, h->num_sms - 16)};
+                   h->bar, std::max(1, (h->num_sms - 16) / h->coop_share)};
   c.pw2 = PanelWork{c.at(L.part2), c.at(L.pz1b), c.at(L.pz2b), c.at(L.gram2), c.at(L.px2), c.at(L.gemm2),
-                    L.gemm2_doubles, h->bar2, h->num_sms};
+                    L.gemm2_doubles, h->bar2, std::max(1, h->num_sms / h->coop_share)};
   c.sw = SvdWork{c.at(L.sW), c.at(L.sJ), c.at(L.sWs), c.at(L.sWh), c.at(L.sTq), c.at(L.sX), c.at(L.sQ), c.at(L.stau),
                  h->info + 2, h->info, c.pw2};
   return c;
@@ -849,6 +1008,188 @@ int64_t lstsq_streamed(utv_handle h, int64_t m, int64_t n, int64_t k, double* A,
   return r;
 }
 
+// ------------------------------------------------------------------------------------------
+// Multi-GPU randUTV least squares: 1D block-cyclic columns (block b, owner(blk) =
+// blk mod P; each rank stores its blocks packed, in order); B / C and the small factors are
+// replicated; the Philox sketch is counter-based, so every rank draws the same G.  Per step i
+// (owner o = i mod P):
+//   Z = sum_p A'_p Y_p                   AllReduce (m' x b), q times                 [a2]
+//   Y rows of every rank                 AllGather; the same QR(Y) on every rank     [a3]
+//   X = sum_p A_p W_V,p (all rows, R1)   AllReduce (m x b); local right update       [a4]
+//   panel QR on o                        Broadcast (W_U, T_U)                        [a5]
+//   fused two-sided update of the local blocks > i (K = 2b, as on one GPU); C := Q_U^T C [a6]
+//   SVD on o                             Broadcast (U_s, V_s, sigma); local updates [a7]
+// V stays factored and replicated (W_V, T_V, V_s are identical on every rank), so X = V z needs
+// no communication; diag(T) is replicated through the sigma broadcasts (rank: no collective);
+// the back substitution is block by block from the bottom with one AllReduce (partial sums of
+// T_{blk, >blk} z) and one Broadcast (z_blk) per block.
+// ------------------------------------------------------------------------------------------
+int64_t dist_local_cols(int64_t n, int64_t b, int P, int p) {
+  const int64_t nb = (n + b - 1) / b;
+  int64_t c = 0;
+  for (int64_t blk = p; blk < nb; blk += P) c += std::min(b, n - blk * b);
+  return c;
+}
+
+int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
+                   double* X, int64_t ldx, const utv_opts& opt) {
+  Comm& comm = *h->comm;
+  const int P = comm.nranks, p = comm.rank;
+  const int64_t b = opt.block, nb = (n + b - 1) / b;
+  const int64_t nloc = dist_local_cols(n, b, P, p);
+  if (opt.flags & (UTV_NULLIFY_T12 | UTV_EXPLICIT_V | UTV_HOST_STREAMED))
+    fail(UTV_ERR_UNSUPPORTED, "the multi-GPU path implements the fast option with factored V only");
+  if ((nloc > 0 && !is_device_ptr(A)) || (k > 0 && (!is_device_ptr(B) || !is_device_ptr(X))))
+    fail(UTV_ERR_ARG, "the multi-GPU path takes device pointers (A = this rank's shard)");
+  cudaStream_t st = h->stream;
+  const int ns = h->num_sms;
+  Ctx c = make_ctx(h, m, n, k, b);
+  const Layout& L = c.L;
+  const int64_t nsteps = nb;
+  const size_t wdbl = factored_w_doubles(n, b), tdbl = (size_t)nsteps * b * b;
+  ensure_buf(&h->vbuf, &h->vbuf_doubles, wdbl + 2 * tdbl + 64);
+  FactoredV fv;
+  fv.W = h->vbuf; fv.T = h->vbuf + wdbl; fv.Vs = fv.T + tdbl;
+  const int64_t Lmax = (nb + P - 1) / P * b;
+  const size_t kk = (size_t)std::max<int64_t>(k, 1);
+  ensure_buf(&h->dbuf, &h->dbuf_doubles, (size_t)Lmax * b * (P + 1) + n + 64 + 2 * (size_t)b * kk + 64);
+  double* Ypad = h->dbuf;
+  double* recv = Ypad + (size_t)Lmax * b;
+  double* dg = recv + (size_t)P * Lmax * b;
+  double* sbuf = dg + n + 64;
+  double* zb = sbuf + (size_t)b * kk;
+  double* flags = zb + (size_t)b * kk;
+  UTV_CUDA(cudaMemsetAsync(h->info, 0, 4 * sizeof(int), st));
+  UTV_CUDA(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
+  if (nloc > 0) launch_check_finite(st, m, nloc, A, lda, h->flag);
+  if (k > 0) launch_check_finite(st, m, k, B, ldb, h->flag);
+  double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *WP = c.at(L.Wv), *Xa = c.at(L.X), *LU = c.at(L.Wu);
+  double *Tu = c.at(L.Tu), *tauu = c.at(L.tauu), *tauv = c.at(L.tauv), *S = c.at(L.S), *Z1 = c.at(L.Z1);
+  double *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp2), *Us = c.at(L.Us), *sig = c.at(L.sig), *Yl = c.at(L.tmp);
+
+  for (int64_t i = 0, j0 = 0; i < nb; ++i, j0 += b) {
+    const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0;
+    const int owner = (int)(i % P);
+    const bool own = p == owner;
+    const int64_t first = i <= p ? 0 : (i - p + P - 1) / P;            // my first block >= i
+    const int64_t lt = first * b, ncl = nloc - lt;                     // my trailing columns
+    const int64_t lr = lt + (own ? bw : 0), nrl = ncl - (own ? bw : 0); // my columns > block i
+    const int64_t ldwp = std::max<int64_t>(ncl, 1);
+    const bool right = np > b;                                          // R5
+    double* X2 = LU;
+    double* Wu = LU + cm(j0, b, m);
+    double* At = A + cm(j0, lt, lda);
+    if (right) {
+      double* Tvs = fv.T + (size_t)i * b * b;
+      launch_sketch(st, opt.seed, i, j0, mp, b, G, mp, ns);                           // a1
+      if (ncl) c.gemm(true, false, ncl, b, mp, 1.0, At, lda, G, mp, 0.0, Yl, ldwp);
+      for (int32_t it = 0; it < opt.power_iters; ++it) {                              // a2 (R7)
+        if (ncl) c.gemm(false, false, mp, b, ncl, 1.0, At, lda, Yl, ldwp, 0.0, Z, mp);
+        else launch_set_zero(st, mp, b, Z, mp);
+        comm.allreduce(Z, (size_t)mp * b, st);
+        if (ncl) c.gemm(true, false, ncl, b, mp, 1.0, At, lda, Z, mp, 0.0, Yl, ldwp);
+      }
+      launch_copy(st, ncl, b, Yl, ldwp, Ypad, Lmax);                                  // AllGather(Y)
+      comm.allgather(Ypad, recv, (size_t)Lmax * b, st);
+      launch_assemble_y(st, np, b, b, i, P, Lmax, recv, Y, np);
+      fv.woff.push_back(fv.woff.empty() ? 0 : fv.woff.back() + (size_t)fv.np.back() * b);
+      fv.j0.push_back(j0); fv.np.push_back(np); fv.has_q.push_back(1);
+      double* Wv = fv.W + fv.woff.back();
+      panel_qr(st, np, b, Y, np, Wv, np, tauv, Tvs, b, c.pw);                          // a3 (same on all)
+      launch_gather_local(st, ncl, b, b, i, P, p, Wv, np, WP, ldwp);                   // my rows of W_V
+      if (ncl) c.gemm(false, false, m, b, ncl, 1.0, A + cm(0, lt, lda), lda, WP, ldwp, 0.0, Xa, m);
+      else launch_set_zero(st, m, b, Xa, m);
+      comm.allreduce(Xa, (size_t)m * b, st);                                          // a4, R1
+      c.gemm(false, false, m, b, b, 1.0, Xa, m, Tvs, b, 0.0, X2, m);
+      if (j0 > 0 && ncl) c.gemm(false, true, j0, ncl, b, -1.0, X2, m, WP, ldwp, 1.0, A + cm(0, lt, lda), lda);
+      if (own) c.gemm(false, true, mp, bw, b, -1.0, X2 + j0, m, WP, ldwp, 1.0, At, lda);
+    }
+    if (own) panel_qr(st, mp, bw, At, lda, Wu, m, tauu, Tu, b, c.pw);                   // a5
+    comm.bcast(LU + cm(0, b, m), (size_t)m * b, owner, st);
+    comm.bcast(Tu, (size_t)b * b, owner, st);
+    if (nrl > 0) {                                                                      // a6, R3
+      double* Ar = A + cm(j0, lr, lda);
+      c.gemm(true, false, bw, nrl, mp, 1.0, Wu, m, Ar, lda, 0.0, Z1, bw);
+      if (right) {
+        double* Wr = WP + (own ? bw : 0);
+        c.gemm(true, false, bw, b, mp, 1.0, Wu, m, X2 + j0, m, 0.0, S, bw);
+        c.gemm(false, true, bw, nrl, b, -1.0, S, bw, Wr, ldwp, 1.0, Z1, bw);
+        c.gemm(true, false, nrl, bw, bw, 1.0, Z1, bw, Tu, b, 0.0, Wr + cm(0, b, ldwp), ldwp);
+        c.gemm(false, true, mp, nrl, 2 * b, -1.0, X2 + j0, m, Wr, ldwp, 1.0, Ar, lda);  // fused, K = 2b
+      } else {
+        c.gemm(true, false, bw, nrl, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+        c.gemm(false, false, mp, nrl, bw, -1.0, Wu, m, Z2, bw, 1.0, Ar, lda);
+      }
+    }
+    if (k > 0) {                                                                        // C := Q_U^T C
+      double* Cr = B + j0;
+      c.gemm(true, false, bw, k, mp, 1.0, Wu, m, Cr, ldb, 0.0, Z1, bw);
+      c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+      c.gemm(false, false, mp, k, bw, -1.0, Wu, m, Z2, bw, 1.0, Cr, ldb);
+    }
+    double* Vsi = fv.Vs + (size_t)i * b * b;                                            // a7
+    if (own) {
+      svd_small(st, bw, At, lda, Us, b, sig, Vsi, b, c.sw);
+      launch_set_diag(st, bw, sig, At, lda);
+      if (j0 > 0) {                                                                     // A01 := A01 V_s
+        c.gemm(false, false, j0, bw, bw, 1.0, A + cm(0, lt, lda), lda, Vsi, b, 0.0, tmp, j0);
+        launch_copy(st, j0, bw, tmp, j0, A + cm(0, lt, lda), lda);
+      }
+    }
+    comm.bcast(Us, (size_t)b * b, owner, st);
+    comm.bcast(Vsi, (size_t)b * b, owner, st);
+    comm.bcast(sig, (size_t)b, owner, st);
+    launch_copy(st, bw, 1, sig, bw, dg + j0, n);
+    if (nrl > 0) {                                                                      // A12 := U_s^T A12
+      double* A12 = A + cm(j0, lr, lda);
+      c.gemm(true, false, bw, nrl, bw, 1.0, Us, b, A12, lda, 0.0, tmp, bw);
+      launch_copy(st, bw, nrl, tmp, bw, A12, lda);
+    }
+    if (k > 0) {                                                                        // C1 := U_s^T C1
+      c.gemm(true, false, bw, k, bw, 1.0, Us, b, B + j0, ldb, 0.0, Z1, bw);
+      launch_copy(st, bw, k, Z1, bw, B + j0, ldb);
+    }
+  }
+  // every rank fails alike: AllReduce the local NaN / Jacobi flags
+  UTV_CUDA(cudaMemcpyAsync(h->h_info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  UTV_CUDA(cudaMemcpyAsync(h->h_info + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  UTV_CUDA(cudaStreamSynchronize(st));
+  const double fl[2] = {(double)h->h_info[2], (double)h->h_info[1]};
+  UTV_CUDA(cudaMemcpyAsync(flags, fl, sizeof(fl), cudaMemcpyHostToDevice, st));
+  comm.allreduce(flags, 2, st);
+  double flo[2] = {0.0, 0.0};
+  UTV_CUDA(cudaMemcpyAsync(flo, flags, sizeof(flo), cudaMemcpyDeviceToHost, st));
+  UTV_CUDA(cudaStreamSynchronize(st));
+  if (flo[0] != 0.0) fail(UTV_ERR_NUMERICAL, "NaN or Inf in A or B (on some rank)");
+  if (flo[1] != 0.0) fail(UTV_ERR_NUMERICAL, "Jacobi SVD of a diagonal block did not converge in 30 sweeps");
+  const int64_t r = finish_factor(c, n, dg, 0, opt.tau, true);                          // a8 (replicated)
+  if (k <= 0) return r;
+  // a9: z = T11^{-1} C(0:r, :) block by block from the bottom
+  double* Zb = c.at(L.zsolve);
+  double* Sp = c.at(L.nY);                                                               // my partial sums
+  double* D = c.at(L.R);
+  if (r > 0) launch_set_zero(st, r, k, Sp, r);
+  for (int64_t blk = r > 0 ? (r - 1) / b : -1; blk >= 0; --blk) {
+    const int64_t j0 = blk * b, j1 = std::min(r, j0 + b), w = j1 - j0;
+    const int o = (int)(blk % P);
+    launch_copy(st, w, k, Sp + j0, r, sbuf, w);
+    comm.allreduce(sbuf, (size_t)w * k, st);                                             // sum_l T_blk,l z_l
+    if (p == o) {
+      const int64_t lc = (blk / P) * b;
+      launch_copy(st, w, k, B + j0, ldb, zb, w);
+      launch_axpy(st, w * k, -1.0, sbuf, zb);
+      launch_copy(st, w, w, A + cm(j0, lc, lda), lda, D, b);
+      launch_trsv_block(st, 0, w, D, b, zb, w, k);
+      if (j0 > 0) c.gemm(false, false, j0, k, w, 1.0, A + cm(0, lc, lda), lda, zb, w, 1.0, Sp, r);
+    }
+    comm.bcast(zb, (size_t)w * k, o, st);
+    launch_copy(st, w, k, zb, w, Zb + j0, r);
+  }
+  solve_factored(c, n, r, nullptr, 0, nullptr, 0, k, X, ldx, fv, b, nullptr, true);      // X = V z (replicated)
+  UTV_CUDA(cudaStreamSynchronize(st));
+  return r;
+}
+
 }  // namespace
 
 extern "C" {
@@ -891,9 +1232,71 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
   return UTV_OK;
 }
 
-utv_status utv_create_dist(utv_handle* handle, int, void*, const void*, int, int) {
-  if (handle) *handle = nullptr;
-  return UTV_ERR_UNSUPPORTED;
+utv_status utv_get_unique_id(void* uid) {
+  if (!uid) return UTV_ERR_ARG;
+  const NcclApi* api = nccl_api();
+  if (!api) return UTV_ERR_NCCL;
+  ncclUniqueId id;
+  if (api->getUniqueId(&id) != ncclSuccess) return UTV_ERR_NCCL;
+  std::memcpy(uid, &id, sizeof(id));
+  return UTV_OK;
+}
+
+utv_status utv_create_dist(utv_handle* handle, int device, void* stream, const void* nccl_uid, int nranks, int rank) {
+  if (!handle) return UTV_ERR_ARG;
+  *handle = nullptr;
+  if (!nccl_uid || nranks < 1 || rank < 0 || rank >= nranks) return UTV_ERR_ARG;
+  utv_handle h = nullptr;
+  utv_status s = utv_create(&h, device, stream);
+  if (s != UTV_OK) return s;
+  s = guarded(h, [&] {
+    const NcclApi* api = nccl_api();
+    if (!api) fail(UTV_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    auto* c = new NcclComm();
+    c->api = api;
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_uid, sizeof(id));
+    h->comm = c;
+    c->check(api->commInitRank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+  });
+  if (s != UTV_OK) {
+    if (h->comm) { delete h->comm; h->comm = nullptr; }   // NcclComm dtor skips a null comm
+    utv_destroy(h);
+    return s;
+  }
+  *handle = h;
+  return UTV_OK;
+}
+
+utv_status utv_create_local_group(utv_handle* handles, int nranks, const int* devices, void* const* streams) {
+  if (!handles || nranks < 1 || !devices) return UTV_ERR_ARG;
+  for (int r = 0; r < nranks; ++r) handles[r] = nullptr;
+  auto g = std::make_shared<LocalGroup>(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    utv_handle h = nullptr;
+    utv_status s = utv_create(&h, devices[r], streams ? streams[r] : nullptr);
+    if (s != UTV_OK) {
+      for (int q = 0; q < r; ++q) { utv_destroy(handles[q]); handles[q] = nullptr; }
+      return s;
+    }
+    int share = 0;
+    for (int q = 0; q < nranks; ++q) share += devices[q] == devices[r];
+    h->coop_share = std::max(1, share);
+    auto* c = new LocalComm();
+    c->g = g;
+    c->nranks = nranks;
+    c->rank = r;
+    h->comm = c;
+    handles[r] = h;
+  }
+  return UTV_OK;
+}
+
+int64_t utv_dist_local_cols(int64_t n, int64_t block, int nranks, int rank) {
+  if (n <= 0 || block < 1 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+  return dist_local_cols(n, block, nranks, rank);
 }
 
 utv_status utv_destroy(utv_handle h) {
@@ -912,6 +1315,8 @@ utv_status utv_destroy(utv_handle h) {
   if (h->ev_done) cudaEventDestroy(h->ev_done);
   if (h->ev_wb) cudaEventDestroy(h->ev_wb);
   cudaFree(h->ooc);
+  cudaFree(h->dbuf);
+  delete h->comm;
   cudaFree(h->bar2);
   cudaFree(h->ws); cudaFree(h->bar); cudaFree(h->info); cudaFree(h->flag); cudaFree(h->d_rank);
   cudaFree(h->vbuf); cudaFree(h->stage); cudaFree(h->nbuf);
@@ -935,6 +1340,7 @@ utv_status utv_factor(utv_handle h, int64_t m, int64_t n, double* A, int64_t lda
                       int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts* opts, int64_t* rank) {
   return guarded(h, [&] {
     check_opts(opts);
+    if (h->comm) fail(UTV_ERR_UNSUPPORTED, "a multi-GPU handle implements utv_lstsq only");
     if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
     if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
     if (n > 0 && !A) fail(UTV_ERR_ARG, "A is NULL");
@@ -974,6 +1380,14 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
     check_ld("lda", lda, m);
     if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
+    if (h->comm) {                                                     // multi-GPU handle
+      const int64_t nloc = n > 0 ? dist_local_cols(n, opts->block, h->comm->nranks, h->comm->rank) : 0;
+      if ((nloc > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
+      if (n == 0) { if (rank) *rank = 0; return; }
+      const int64_t r = lstsq_dist(h, m, n, k, A, lda, B, ldb, X, ldx, *opts);
+      if (rank) *rank = r;
+      return;
+    }
     if ((n > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
     if (n == 0) { if (rank) *rank = 0; return; }
     if (opts->flags & UTV_HOST_STREAMED) {
@@ -1210,3 +1624,15 @@ utv_status utv_profile_read(utv_handle h, utv_prof_entry* out) {
 }
 
 }  // extern "C"
+
+// diagnostics only (not part of utv.h): run one collective of a multi-GPU handle on a device buffer
+// (op 0 = AllReduce(sum) in place, 1 = Broadcast from `root`, 2 = AllGather of n into recv).
+extern "C" utv_status utv_debug_collective(utv_handle h, int op, double* buf, int64_t n, int root, double* recv) {
+  return guarded(h, [&] {
+    if (!h->comm) fail(UTV_ERR_ARG, "not a multi-GPU handle");
+    if (op == 0) h->comm->allreduce(buf, (size_t)n, h->stream);
+    else if (op == 1) h->comm->bcast(buf, (size_t)n, root, h->stream);
+    else h->comm->allgather(buf, recv, (size_t)n, h->stream);
+    UTV_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}

@@ -1,0 +1,143 @@
+"""Native multi-GPU path (utv_create_local_group / utv_create_dist) against the oracle.
+
+The in-process group runs P ranks as host threads on ONE GPU (each rank its own handle and
+stream, collectives combined in rank order), so the block-cyclic orchestration, the collectives'
+payloads and the owner logic are exercised at P = 2..5 on the single GPU this round has; the NCCL
+communicator is checked at P = 1 (NCCL refuses two ranks on one device).  Gates: r identical on
+every rank and equal to the oracle's, X identical on every rank and within 1e-9 of the oracle.
+"""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import utv_inputs as gen
+from paper_2408_05238_b200 import dist as D
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def utv():
+    from paper_2408_05238_b200 import build
+    build.build()
+    import paper_2408_05238_b200 as m
+    return m
+
+
+def dev(a):
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    return torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+
+
+def run_group(utv, handles, A, B, b, q, seed):
+    P = len(handles)
+    m, n = A.shape
+    Ad = dev(A)
+    shards = [utv.colmajor(D.scatter_columns(Ad, b, P, p).clone()) for p in range(P)]
+    for p in range(P):
+        assert shards[p].shape[1] == utv.dist_local_cols(n, b, P, p)
+    Bs = [dev(B) for _ in range(P)]
+    Xs = [utv.colmajor_empty(n, Bs[0].shape[1]) for _ in range(P)]
+    torch.cuda.synchronize()
+    out = [None] * P
+    err = [None] * P
+    opts = utv.Opts(block=b, power_iters=q, tau=1e-10, seed=seed)
+
+    def work(p):
+        try:
+            Ap = shards[p] if shards[p].shape[1] > 0 else utv.colmajor_empty(m, 1)
+            out[p] = handles[p].lstsq(Ap, Bs[p], Xs[p], opts)
+        except Exception as e:          # noqa: BLE001 -- re-raised below
+            err[p] = e
+
+    ts = [threading.Thread(target=work, args=(p,)) for p in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in ts), "a rank hung"
+    for e in err:
+        if e is not None:
+            raise e
+    torch.cuda.synchronize()
+    return [X.cpu().numpy() for X in Xs], out
+
+
+@pytest.mark.parametrize("P,m,n,r,b,q,k", [
+    (2, 600, 600, 300, 64, 1, 2),
+    (3, 700, 550, 260, 64, 2, 3),     # ragged last block
+    (4, 300, 300, 150, 32, 1, 1),
+    (5, 130, 100, 40, 32, 1, 1),      # more ranks than blocks: rank 4 holds no column
+    (2, 2048, 2048, 1000, 256, 2, 1),
+])
+def test_local_group_matches_oracle(utv, P, m, n, r, b, q, k):
+    M = gen.GpMatrix(m, n, r, seed=m + n + P)
+    B, X0 = M.known_rhs(k=k)
+    B = B.reshape(m, -1)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=11)
+    hs = utv.local_group(P)
+    try:
+        Xs, rs = run_group(utv, hs, M.A, B, b, q, 11)
+    finally:
+        for h in hs:
+            h.close()
+    assert all(x == ro == r for x in rs), (rs, ro)
+    for X in Xs:
+        assert np.array_equal(X, Xs[0])                     # replicated result, bit-identical
+    assert np.linalg.norm(Xs[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)
+    assert np.linalg.norm(Xs[0] - X0) <= 1e-10 * np.linalg.norm(X0)
+
+
+def test_local_group_single_rank_equals_in_core(utv):
+    """P = 1: the multi-GPU orchestration with no peers == the single-GPU path (rounding only)."""
+    m, n, r, b, q = 900, 700, 333, 128, 2
+    M = gen.GpMatrix(m, n, r, seed=2)
+    B, _ = M.known_rhs(k=2)
+    hs = utv.local_group(1)
+    try:
+        Xs, rs = run_group(utv, hs, M.A, B, b, q, 4)
+    finally:
+        hs[0].close()
+    Xd, rd = utv.lstsq(dev(M.A), dev(B), utv.Opts(block=b, power_iters=q, tau=1e-10, seed=4))
+    Xd = Xd.cpu().numpy()
+    assert rs[0] == rd == r
+    assert np.linalg.norm(Xs[0] - Xd) <= 1e-12 * np.linalg.norm(Xd)
+
+
+def test_nccl_single_rank(utv):
+    """utv_create_dist through NCCL (nranks = 1 on the one GPU available)."""
+    uid = utv.get_unique_id()
+    assert len(uid) == 128
+    h = utv.dist_handle(uid, 1, 0)
+    try:
+        m, n, r, b = 500, 400, 180, 64
+        M = gen.GpMatrix(m, n, r, seed=8)
+        B, X0 = M.known_rhs(k=1)
+        Xo, ro = oracle.lstsq(M.A, B, b=b, q=1, tau=1e-10, seed=3)
+        Xs, rs = run_group(utv, [h], M.A, B.reshape(m, 1), b, 1, 3)
+    finally:
+        h.close()
+    assert rs[0] == ro == r
+    assert np.linalg.norm(Xs[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
+def test_dist_handle_rejects_factor_and_flags(utv):
+    hs = utv.local_group(1)
+    h = hs[0]
+    try:
+        A = utv.colmajor_empty(64, 64).zero_()
+        with pytest.raises(utv.UtvError) as e:
+            h.factor(A)
+        assert e.value.status == utv.UTV_ERR_UNSUPPORTED
+        B = utv.colmajor_empty(64, 1).zero_()
+        X = utv.colmajor_empty(64, 1)
+        with pytest.raises(utv.UtvError) as e:
+            h.lstsq(A, B, X, utv.Opts(block=16, flags=utv.UTV_NULLIFY_T12))
+        assert e.value.status == utv.UTV_ERR_UNSUPPORTED
+    finally:
+        h.close()
