@@ -18,6 +18,7 @@ struct ProfRec {
   cudaEvent_t e0, e1;
   int64_t M = 0, N = 0, K = 0;   // GEMM shape (diagnostics)
   int tag = 0;                   // GEMM: ta | tb << 1 | cfg << 2 | splits << 8
+  cudaStream_t stream = nullptr;  // timeline diagnostics (prof_dump)
 };
 
 struct Profiler {
