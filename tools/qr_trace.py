@@ -8,9 +8,9 @@ for m in (50000, 2000):
     for _ in range(2):
         P = P0.clone(); h.hqr(P)
     torch.cuda.synchronize()
-    buf = (ctypes.c_longlong * 512)()
+    buf = (ctypes.c_longlong * 1024)()
     L.utv_debug_qr_trace(buf)
-    t = np.array(buf).reshape(64, 8)[:32]
+    t = np.array(buf[:512]).reshape(64, 8)[:32]
     # phases: 0 loop start, 3 after block reduce, 4 after barrier, 1 after partial reduce, 2 after dlarfg/T
     d = lambda a, b: t[:, b] - t[:, a]
     print(m, "cycles/col: reduce_store %.0f barrier %.0f partials %.0f dlarfg+T %.0f update %.0f total %.0f" % (
