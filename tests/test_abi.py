@@ -70,3 +70,34 @@ def test_oracle_not_imported_by_product():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text and "utv_oracle" not in text, f
+
+
+def test_sass_uses_tma_and_mbarriers(libpath):
+    """The GEMM operand tiles are staged by TMA (UTMALDG) with mbarrier completion (SYNCS)."""
+    out = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
+    assert "UTMALDG" in out
+    assert "SYNCS.ARRIVE.TRANS64" in out
+
+
+def test_dist_local_cols_matches_python_layout(libpath):
+    """utv_dist_local_cols (C) == the block-cyclic layout of paper_2408_05238_b200.dist (no GPU)."""
+    import paper_2408_05238_b200 as utv
+    from paper_2408_05238_b200 import dist as D
+    for n, b, P in ((1000, 64, 3), (600, 64, 2), (100, 32, 5), (50000, 256, 8), (257, 256, 4)):
+        cols = [utv.dist_local_cols(n, b, P, p) for p in range(P)]
+        assert cols == [D.local_ncols(n, b, P, p) for p in range(P)]
+        assert sum(cols) == n
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the CPU oracle arm) prints one JSON line with the contract keys."""
+    import json
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--ref-n", "256"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "impl", "cpu_baseline",
+                "e2e", "config"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
