@@ -176,7 +176,7 @@ struct utv_handle_s {
   unsigned* bar = nullptr;       // grid-barrier state: [0] count, [1] generation (main stream)
   unsigned* bar2 = nullptr;      // grid-barrier state of the SVD side stream
   cudaStream_t side = nullptr;   // a7 (small SVD + its 4 updates) overlaps the next step's sketch
-  cudaEvent_t ev_panel = nullptr, ev_svd = nullptr;
+  cudaEvent_t ev_panel = nullptr, ev_svd = nullptr, ev_us = nullptr;
   int* info = nullptr;           // Jacobi sweeps / failure flag
   int* flag = nullptr;           // finiteness flag
   int64_t* d_rank = nullptr;
@@ -254,7 +254,7 @@ void ensure_buf(double** p, size_t* have, size_t need) {
 
 // Workspace layout for one factorization (offsets in doubles).
 struct Layout {
-  size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, S, Tu, tauu, Z1, Z2, tmp, R, Us, Vs, sig;
+  size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, S, Tu, tauu, Z1, Z2, tmp, R, Us, Us2, Vs, sig;
   size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve;
   size_t part2, pz1b, pz2b, gram2, px2, gemm2, tmp2;
   size_t nM, nW, ntau, nT, nWt, nY, nY2;
@@ -285,6 +285,7 @@ Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
   L.tmp = take(std::max<size_t>(mx * b, (size_t)b * nk));
   L.R = take((size_t)b * b);
   L.Us = take((size_t)b * b);
+  L.Us2 = take((size_t)b * b);
   L.Vs = take((size_t)b * b);
   L.sig = take(b);
   L.sW = take((size_t)b * b);
@@ -425,6 +426,9 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
          *sig = c.at(L.sig);
   cudaStream_t sd = c.side;
   bool svd_pending = false;
+  bool us_pending = false, us_applied = false;      // deferred A12 := U_s^T A12 (see below)
+  int64_t us_j0 = 0, us_bw = 0;
+  int us_buf = 0;
   // the side stream must not start before the work enqueued on the main stream so far
   UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
   UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
@@ -456,7 +460,6 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
         fv->j0.push_back(j0); fv->np.push_back(np); fv->has_q.push_back(1);
         launch_copy(st, np, b, WVZ, np, fv->W + fv->woff.back(), np);
       }
-      if (svd_pending) UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));             // A12 of step-1
       double* Ac = A + cm(0, j0, lda);                                                 // a4, R1: all rows
       c.gemm(false, false, m, b, np, 1.0, Ac, lda, WVZ, np, 0.0, X, m);               // X = A W_V
       c.gemm(false, false, m, b, b, 1.0, X, m, Tvs, b, 0.0, X2, m);                   // X2 = X T_V
@@ -498,6 +501,21 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
       c.gemm(false, false, m, bw, bw, 1.0, X, m, Tu, b, 0.0, Xv2, m);
       c.gemm(false, true, m, mp, bw, -1.0, Xv2, m, Wu, m, 1.0, Uc, ldu);
     }
+    // ---- deferred A12 := U_s^T A12 of the PREVIOUS step (main stream) ----
+    // Rows j0':j0'+b of the trailing columns (step i-1's A12) are only right-multiplied after step
+    // i-1 (right updates of the top rows; nothing else reads them), and a left multiplication
+    // commutes with those, so U_s^T is applied here -- one step late -- instead of making the X
+    // GEMM of this step wait for the side-stream SVD (the SVD now has a whole step to finish).
+    if (us_pending) {
+      UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
+      double* A12p = A + cm(us_j0, us_j0 + us_bw, lda);
+      const double* Usp = (us_buf ? c.at(L.Us2) : c.at(L.Us));
+      c.gemm(true, false, us_bw, n - us_j0 - us_bw, us_bw, 1.0, Usp, b, A12p, lda, 0.0, c.at(L.tmp), us_bw);
+      launch_copy(st, us_bw, n - us_j0 - us_bw, c.at(L.tmp), us_bw, A12p, lda);
+      UTV_CUDA(cudaEventRecord(c.h->ev_us, st));
+      us_pending = false;
+      us_applied = true;
+    }
     // ---- small SVD and the four updates ----
     // a7 on the side stream: it only needs R (this step's panel) and touches A11, A01, A12,
     // V(:, block), C(block, :), U(:, block).  The next step's sketch, power iterations and
@@ -506,17 +524,19 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
     UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
     double* Vsi = fv ? fv->Vs + (size_t)step * b * b : Vs;                             // V_s (kept if factored)
-    svd_small(sd, bw, Ap, lda, Us, b, sig, Vsi, b, c.sw);                              // a7
+    double* Usi = (step & 1) ? c.at(L.Us2) : Us;                                        // kept until applied
+    svd_small(sd, bw, Ap, lda, Usi, b, sig, Vsi, b, c.sw);                             // a7
     launch_set_diag(sd, bw, sig, Ap, lda);
     if (j0 > 0) {                                                                       // A01 := A01 V_s
+      // A01's last b rows were just rotated by the deferred U_s^T of step i-1 (main stream)
+      if (us_applied) UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_us, 0));
       double* A01 = A + cm(0, j0, lda);
       c.gemm_side(false, false, j0, bw, bw, 1.0, A01, lda, Vsi, b, 0.0, tmp, j0);
       launch_copy(sd, j0, bw, tmp, j0, A01, lda);
     }
     if (nr > 0) {                                                                       // A12 := U_s^T A12
-      double* A12 = A + cm(j0, j0 + bw, lda);
-      c.gemm_side(true, false, bw, nr, bw, 1.0, Us, b, A12, lda, 0.0, tmp, bw);
-      launch_copy(sd, bw, nr, tmp, bw, A12, lda);
+      us_pending = true;                                                                // next step, main
+      us_j0 = j0; us_bw = bw; us_buf = (int)(step & 1);
     }
     if (V) {                                                                            // V1 := V1 V_s
       double* V1 = V + cm(0, j0, ldv);
@@ -525,18 +545,24 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     }
     if (B && k > 0) {                                                                   // C1 := U_s^T C1
       double* C1 = B + cm(j0, 0, ldb);
-      c.gemm_side(true, false, bw, k, bw, 1.0, Us, b, C1, ldb, 0.0, tmp, bw);
+      c.gemm_side(true, false, bw, k, bw, 1.0, Usi, b, C1, ldb, 0.0, tmp, bw);
       launch_copy(sd, bw, k, tmp, bw, C1, ldb);
     }
     if (U) {                                                                            // U1 := U1 U_s
       double* U1 = U + cm(0, j0, ldu);
-      c.gemm_side(false, false, m, bw, bw, 1.0, U1, ldu, Us, b, 0.0, tmp, m);
+      c.gemm_side(false, false, m, bw, bw, 1.0, U1, ldu, Usi, b, 0.0, tmp, m);
       launch_copy(sd, m, bw, tmp, m, U1, ldu);
     }
     UTV_CUDA(cudaEventRecord(c.h->ev_svd, sd));
     svd_pending = true;
   }
   if (svd_pending) UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
+  if (us_pending) {                                                                     // the last A12
+    double* A12p = A + cm(us_j0, us_j0 + us_bw, lda);
+    const double* Usp = (us_buf ? c.at(L.Us2) : c.at(L.Us));
+    c.gemm(true, false, us_bw, n - us_j0 - us_bw, us_bw, 1.0, Usp, b, A12p, lda, 0.0, c.at(L.tmp), us_bw);
+    launch_copy(st, us_bw, n - us_j0 - us_bw, c.at(L.tmp), us_bw, A12p, lda);
+  }
   if (m > n) launch_set_zero(st, m - n, n, A + n, lda);   // rows below T (already 0 by R13; kept explicit)
 }
 
@@ -1221,6 +1247,7 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
     UTV_CUDA(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_panel, cudaEventDisableTiming));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_svd, cudaEventDisableTiming));
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_us, cudaEventDisableTiming));
     UTV_CUDA(cudaMalloc((void**)&h->info, 64 * sizeof(int)));
     UTV_CUDA(cudaMalloc((void**)&h->flag, sizeof(int)));
     UTV_CUDA(cudaMalloc((void**)&h->d_rank, sizeof(int64_t)));
@@ -1306,6 +1333,7 @@ utv_status utv_destroy(utv_handle h) {
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->ev_panel) cudaEventDestroy(h->ev_panel);
   if (h->ev_svd) cudaEventDestroy(h->ev_svd);
+  if (h->ev_us) cudaEventDestroy(h->ev_us);
   if (h->h2d) { cudaStreamSynchronize(h->h2d); cudaStreamDestroy(h->h2d); }
   if (h->d2h) { cudaStreamSynchronize(h->d2h); cudaStreamDestroy(h->d2h); }
   for (int s = 0; s < utv_handle_s::kStg; ++s) {
