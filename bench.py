@@ -378,7 +378,8 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "time_to_solution_s": t, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: square n={n} rank {r_true}, b={b}, q={q}, k={k} (paper generator "
+        "config": {"workload": (f"{args.config}: square n={n}" if m == n else f"{args.config}: tall m={m} x n={n}")
+                               + f" rank {r_true}, b={b}, q={q}, k={k} (paper generator "
                                "P:2436-2448, known min-norm solution)", "m": m, "n": n, "rank": r_true, "block": b,
                    "power_iters": q, "rhs": k,
                    "parallelism": f"blockcyclic{world}" if use_dist else "single",
