@@ -87,3 +87,31 @@ def test_residual_identity_and_sampled_T(utv):
         i, j = int(rng.integers(0, m)), int(rng.integers(0, n))
         tij = float(U[:, i] @ (A0 @ V[:, j]))
         assert abs(float(A[i, j]) - tij) <= 1e-12 * A0.norm().item()
+
+
+def test_cfg2_streamed_out_of_core(utv, monkeypatch):
+    """configs[1] through the out-of-core mode (UTV_HOST_STREAMED): A in pinned host memory, only
+    8192 of the 20000 columns resident in HBM; known min-norm solution and exact rank."""
+    monkeypatch.setenv("UTV_OOC_MAX_RESIDENT_COLS", "8192")
+    m = n = 20000
+    r, b, q = 10000, 256, 2
+    dev = torch.device("cuda:0")
+    At, Bm, X0 = gen.gp_torch(m, n, r, seed=gen.MATRIX_SEED, device=dev, k=1)
+    A0 = At.t()
+    Ah = utv.colmajor_empty(m, n, device="cpu", pin_memory=True)
+    Ah.copy_(A0)
+    Bh = utv.colmajor(Bm).cpu()
+    B0 = utv.colmajor(Bm).clone()
+    Xh = utv.colmajor_empty(n, 1, device="cpu", pin_memory=True)
+    h = utv.Handle(0)
+    rank = h.lstsq(Ah, Bh, Xh, utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED,
+                                          flags=utv.UTV_HOST_STREAMED))
+    st = h.stream_stats()
+    X = Xh.to(dev)
+    rel = ((X - X0).norm() / X0.norm()).item()
+    R = A0 @ X - B0
+    ne = ((A0.t() @ R).norm() / (A0.norm() ** 2 * X.norm())).item()
+    assert rank == r
+    assert rel <= 1e-10, rel
+    assert ne <= 1e-12, ne
+    assert st["resident_cols"] == n - (n - 8192 + b - 1) // b * b and st["h2d_bytes"] > 8 * m * n
