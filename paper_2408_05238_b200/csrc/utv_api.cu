@@ -254,7 +254,7 @@ void ensure_buf(double** p, size_t* have, size_t need) {
 
 // Workspace layout for one factorization (offsets in doubles).
 struct Layout {
-  size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, S, Tu, tauu, Z1, Z2, tmp, R, Us, Us2, Vs, sig;
+  size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, S, Tu, tauu, Z1, Z2, tmp, R, Us, Us2, Vs, sig, sig2;
   size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve;
   size_t part2, pz1b, pz2b, gram2, px2, gemm2, tmp2;
   size_t nM, nW, ntau, nT, nWt, nY, nY2;
@@ -288,6 +288,7 @@ Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
   L.Us2 = take((size_t)b * b);
   L.Vs = take((size_t)b * b);
   L.sig = take(b);
+  L.sig2 = take(b);
   L.sW = take((size_t)b * b);
   L.sJ = take((size_t)b * b);
   L.sWs = take((size_t)b * b);
@@ -1093,6 +1094,32 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   double *Tu = c.at(L.Tu), *tauu = c.at(L.tauu), *tauv = c.at(L.tauv), *S = c.at(L.S), *Z1 = c.at(L.Z1);
   double *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp2), *Us = c.at(L.Us), *sig = c.at(L.sig), *Yl = c.at(L.tmp);
 
+  bool pend = false, us_applied = false;             // deferred SVD application (see a7 below)
+  int64_t p_i = 0, p_j0 = 0, p_bw = 0, p_lr = 0, p_nrl = 0;
+  int p_owner = 0;
+  auto apply_pending = [&]() {
+    if (!pend) return;
+    if (p == p_owner) UTV_CUDA(cudaStreamWaitEvent(st, h->ev_svd, 0));
+    double* Usp = (p_i & 1) ? c.at(L.Us2) : Us;
+    double* sgp = (p_i & 1) ? c.at(L.sig2) : sig;
+    double* Vsp = fv.Vs + (size_t)p_i * b * b;
+    comm.bcast(Usp, (size_t)b * b, p_owner, st);
+    comm.bcast(Vsp, (size_t)b * b, p_owner, st);
+    comm.bcast(sgp, (size_t)b, p_owner, st);
+    launch_copy(st, p_bw, 1, sgp, p_bw, dg + p_j0, n);
+    if (p_nrl > 0) {                                                                    // A12 := U_s^T A12
+      double* A12 = A + cm(p_j0, p_lr, lda);
+      c.gemm(true, false, p_bw, p_nrl, p_bw, 1.0, Usp, b, A12, lda, 0.0, Yl, p_bw);
+      launch_copy(st, p_bw, p_nrl, Yl, p_bw, A12, lda);
+    }
+    if (k > 0) {                                                                        // C1 := U_s^T C1
+      c.gemm(true, false, p_bw, k, p_bw, 1.0, Usp, b, B + p_j0, ldb, 0.0, Z1, p_bw);
+      launch_copy(st, p_bw, k, Z1, p_bw, B + p_j0, ldb);
+    }
+    UTV_CUDA(cudaEventRecord(h->ev_us, st));
+    us_applied = true;
+    pend = false;
+  };
   for (int64_t i = 0, j0 = 0; i < nb; ++i, j0 += b) {
     const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0;
     const int owner = (int)(i % P);
@@ -1153,29 +1180,30 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
       c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
       c.gemm(false, false, mp, k, bw, -1.0, Wu, m, Z2, bw, 1.0, Cr, ldb);
     }
-    double* Vsi = fv.Vs + (size_t)i * b * b;                                            // a7
+    // a7: the SVD of step i runs on the owner's side stream; its results are broadcast and applied
+    // at the end of step i+1 (same point in every rank's sequence of collectives), so no rank waits
+    // for the Jacobi: A12 := U_s^T A12 commutes with the intervening right updates (as on one GPU),
+    // V_s and sigma are only needed by the solve, U_s^T C1 touches rows no later step reads.
+    apply_pending();
     if (own) {
-      svd_small(st, bw, At, lda, Us, b, sig, Vsi, b, c.sw);
-      launch_set_diag(st, bw, sig, At, lda);
+      double* Vsi = fv.Vs + (size_t)i * b * b;
+      double* Usi = (i & 1) ? c.at(L.Us2) : Us;
+      double* sgi = (i & 1) ? c.at(L.sig2) : sig;
+      UTV_CUDA(cudaEventRecord(h->ev_panel, st));
+      UTV_CUDA(cudaStreamWaitEvent(c.side, h->ev_panel, 0));
+      svd_small(c.side, bw, At, lda, Usi, b, sgi, Vsi, b, c.sw);
+      launch_set_diag(c.side, bw, sgi, At, lda);
       if (j0 > 0) {                                                                     // A01 := A01 V_s
-        c.gemm(false, false, j0, bw, bw, 1.0, A + cm(0, lt, lda), lda, Vsi, b, 0.0, tmp, j0);
-        launch_copy(st, j0, bw, tmp, j0, A + cm(0, lt, lda), lda);
+        if (us_applied) UTV_CUDA(cudaStreamWaitEvent(c.side, h->ev_us, 0));         // its rows j0-b:j0
+        c.gemm_side(false, false, j0, bw, bw, 1.0, A + cm(0, lt, lda), lda, Vsi, b, 0.0, tmp, j0);
+        launch_copy(c.side, j0, bw, tmp, j0, A + cm(0, lt, lda), lda);
       }
+      UTV_CUDA(cudaEventRecord(h->ev_svd, c.side));
     }
-    comm.bcast(Us, (size_t)b * b, owner, st);
-    comm.bcast(Vsi, (size_t)b * b, owner, st);
-    comm.bcast(sig, (size_t)b, owner, st);
-    launch_copy(st, bw, 1, sig, bw, dg + j0, n);
-    if (nrl > 0) {                                                                      // A12 := U_s^T A12
-      double* A12 = A + cm(j0, lr, lda);
-      c.gemm(true, false, bw, nrl, bw, 1.0, Us, b, A12, lda, 0.0, tmp, bw);
-      launch_copy(st, bw, nrl, tmp, bw, A12, lda);
-    }
-    if (k > 0) {                                                                        // C1 := U_s^T C1
-      c.gemm(true, false, bw, k, bw, 1.0, Us, b, B + j0, ldb, 0.0, Z1, bw);
-      launch_copy(st, bw, k, Z1, bw, B + j0, ldb);
-    }
+    pend = true;
+    p_i = i; p_j0 = j0; p_bw = bw; p_owner = owner; p_lr = lr; p_nrl = nrl;
   }
+  apply_pending();
   // every rank fails alike: AllReduce the local NaN / Jacobi flags
   UTV_CUDA(cudaMemcpyAsync(h->h_info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   UTV_CUDA(cudaMemcpyAsync(h->h_info + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
