@@ -84,7 +84,8 @@ utv_status utv_create_dist(utv_handle* handle, int device, void* stream, const v
 /* One process, several ranks (one host thread per handle): handles[r] is rank r of an in-process
  * group on devices[r] with streams[r] (NULL = legacy default streams).  Collectives rendezvous on
  * the host and combine the peers' device buffers in rank order; each handle must be driven by its
- * own thread.  Destroy each handle with utv_destroy. */
+ * own thread.  If one rank's call fails, its peers' calls return UTV_ERR_NCCL instead of waiting
+ * forever, and the group stays unusable (destroy it).  Destroy each handle with utv_destroy. */
 utv_status utv_create_local_group(utv_handle* handles, int nranks, const int* devices,
                                   void* const* streams);
 

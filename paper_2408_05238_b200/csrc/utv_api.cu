@@ -28,6 +28,7 @@ using namespace utv;
 struct Comm {
   int nranks = 1, rank = 0;
   virtual ~Comm() {}
+  virtual void abort() {}          // a failing rank releases its peers (in-process groups)
   virtual void allreduce(double* buf, size_t n, cudaStream_t st) = 0;
   virtual void bcast(double* buf, size_t n, int root, cudaStream_t st) = 0;
   virtual void allgather(const double* send, double* recv, size_t n, cudaStream_t st) = 0;
@@ -101,18 +102,26 @@ struct LocalGroup {
   std::condition_variable cv;
   int arrived = 0;
   uint64_t gen = 0;
+  bool aborted = false;            // set by a rank whose call failed: every barrier then throws
   std::vector<const double*> ptr;
   explicit LocalGroup(int n_) : n(n_), ptr(n_, nullptr) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    if (aborted) throw CommError{"a peer rank of the in-process group failed"};
     const uint64_t g = gen;
     if (++arrived == n) {
       arrived = 0;
       ++gen;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return gen != g; });
+      cv.wait(lk, [&] { return gen != g || aborted; });
+      if (gen == g) throw CommError{"a peer rank of the in-process group failed"};
     }
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
   }
 };
 
@@ -160,6 +169,7 @@ struct LocalComm : Comm {
     UTV_CUDA(cudaStreamSynchronize(st));
     g->barrier();
   }
+  void abort() override { g->abort(); }
   ~LocalComm() override {
     if (tmp) cudaFree(tmp);
   }
@@ -220,7 +230,12 @@ utv_status guarded(utv_handle h, F&& f) {
       explicit ProfBind(Profiler* p) { g_prof = p; }
       ~ProfBind() { g_prof = nullptr; }
     } bind(h->prof.on ? &h->prof : nullptr);
-    f();
+    try {
+      f();
+    } catch (...) {
+      if (h->comm) h->comm->abort();
+      throw;
+    }
     h->last_error.clear();
     return UTV_OK;
   } catch (const ApiError& e) {

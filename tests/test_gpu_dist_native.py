@@ -141,3 +141,33 @@ def test_dist_handle_rejects_factor_and_flags(utv):
         assert e.value.status == utv.UTV_ERR_UNSUPPORTED
     finally:
         h.close()
+
+
+def test_local_group_failing_rank_releases_peers(utv):
+    """A rank whose call fails (bad argument) aborts the group: its peers get UTV_ERR_NCCL, no hang."""
+    hs = utv.local_group(2)
+    try:
+        m, n, b = 256, 256, 64
+        A = [utv.colmajor_empty(m, utv.dist_local_cols(n, b, 2, p)).normal_() for p in range(2)]
+        B = [utv.colmajor_empty(m, 1).normal_() for _ in range(2)]
+        X = [utv.colmajor_empty(n, 1) for _ in range(2)]
+        torch.cuda.synchronize()
+        st = [None, None]
+
+        def work(p):
+            try:                                             # rank 1: tau outside [0, 1) -> UTV_ERR_ARG
+                hs[p].lstsq(A[p], B[p], X[p], utv.Opts(block=b, power_iters=1, tau=0.5 if p == 0 else 2.0))
+                st[p] = 0
+            except utv.UtvError as e:
+                st[p] = e.status
+
+        ts = [threading.Thread(target=work, args=(p,)) for p in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=120)
+        assert not any(t.is_alive() for t in ts), "a rank hung"
+        assert st[1] == utv.UTV_ERR_ARG and st[0] == utv.UTV_ERR_NCCL, st
+    finally:
+        for h in hs:
+            h.close()
