@@ -392,6 +392,7 @@ def run_ours(args):
         "executed_tflops": executed_tflops, "executed_flops": F_exec,
         "v_mode": "factored (SURVEY 8(f) #4)" if factored else "explicit",
         "frac_of_fp64_peak": executed_tflops / (world * peak),
+        "frac_of_fp64_datasheet": executed_tflops / (world * 40.0),   # nominal B200 FP64 tensor 40 TF/s (HGX spec)
         "fp64_peak_tflops": peak, "f_alg": F, "rank": r, "rank_ok": r == r_true, "rel_err_x0": rel_err,
         "roofline": {"kernel": "dgemm_tma_kernel (TMA-fed FP64 mma.sync DMMA): the >= 4 GFLOP launches on the "
                                "critical-path stream (sketch products, X = A W_V, trailing updates)",
