@@ -371,6 +371,8 @@ Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
   c.w = h->ws;
   const Layout& L = c.L;
   c.side = h->side;
+  static const bool svd_inline = [] { const char* e = std::getenv("UTV_SVD_INLINE"); return e && e[0] == '1'; }();
+  if (svd_inline) c.side = h->stream;               // diagnostics: no side-stream overlap
   // the main-stream panel kernels leave 16 SMs free for the concurrent side-stream Jacobi
   // Cooperative (grid-barrier) panel kernels: ranks of an in-process group that share a device split
   // its SMs, so that all their grids stay co-resident even when launched at the same time.
