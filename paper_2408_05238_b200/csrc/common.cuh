@@ -2,6 +2,7 @@
 // Product code: nothing here is shared with oracle/ (the CPU checker).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -27,6 +28,20 @@ struct CudaError {
     cudaError_t e_ = (x);                                                   \
     if (e_ != cudaSuccess) throw ::utv::CudaError{e_, #x, __LINE__};        \
   } while (0)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device: function attributes live in
+// each device's context, so a process-wide "done" flag would leave a second device unset (handles
+// of an in-process group on several GPUs).  Racing threads may both set it, which is harmless.
+template <typename K>
+inline void ensure_smem_attr(K kern, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  UTV_CUDA(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  UTV_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bytes));
+  done.fetch_or(bit, std::memory_order_release);
+}
 
 // Column-major element access.
 __host__ __device__ __forceinline__ size_t cm(int64_t i, int64_t j, int64_t ld) {

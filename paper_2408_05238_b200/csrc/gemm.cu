@@ -559,12 +559,9 @@ void launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, co
               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splits, int64_t kc,
               double* partial) {
   using CF = Cfg<TA, TB, ID>;
-  static bool attr_set = false;
+  static std::atomic<unsigned long long> attr_set{0};
   auto kern = dgemm_dmma_kernel<TA, TB, VEC, ID>;
-  if (!attr_set) {
-    UTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
-    attr_set = true;
-  }
+  ensure_smem_attr(kern, (int)CF::SMEM, attr_set);
   dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + CF::BM - 1) / CF::BM)), 1u, (unsigned)splits);
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial);
   UTV_CUDA(cudaGetLastError());
@@ -628,12 +625,9 @@ bool launch_tma_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   // B operand (K x N): !TB -> stored K x N (K-major); TB -> stored N x K (MN-major)
   if (!make_tmap(&tb_map, B, TB ? N : K, TB ? K : N, ldb, TB, CF::BN, &b3)) return false;
   const int mn_3d = (a3 ? 1 : 0) | (b3 ? 2 : 0);
-  static bool attr_set = false;
+  static std::atomic<unsigned long long> attr_set{0};
   auto kern = dgemm_tma_kernel<TA, TB, ID>;
-  if (!attr_set) {
-    UTV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
-    attr_set = true;
-  }
+  ensure_smem_attr(kern, (int)CF::SMEM, attr_set);
   dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + CF::BM - 1) / CF::BM)), 1u, (unsigned)splits);
   kern<<<grid, CF::THREADS, CF::SMEM, st>>>(ta_map, tb_map, M, N, K, alpha, beta, C, ldc, kc, partial, mn_3d);
   UTV_CUDA(cudaGetLastError());

@@ -273,12 +273,8 @@ void svd_small(cudaStream_t st, int64_t bw64, const double* R, int64_t ldr, doub
   fro2_kernel<<<1, 1024, 0, st>>>(bw, sw.W, sw.X);   // X[0] = ||R||_F^2 (scratch)
   UTV_CUDA(cudaGetLastError());
   UTV_CUDA(cudaMemsetAsync(sw.rot, 0, sizeof(int) * kMaxSweeps, st));
-  static bool attr = false;
-  if (!attr) {
-    UTV_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  4 * JBLK * 256 * (int)sizeof(double)));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_smem_attr(jacobi_kernel, 4 * JBLK * 256 * (int)sizeof(double), attr);
   int P = (bw + 2 * JBLK - 1) / (2 * JBLK);
   size_t smem = (size_t)4 * JBLK * bw * sizeof(double);
   int bwv = bw;

@@ -292,12 +292,8 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
                     (void*)&pw.part, (void*)&pw.bar};
     {
       ProfScope prof(st, kProfPanel, 1, 2.0 * (double)R * nb * nb, 16.0 * (double)R * nb);
-      static bool attr = false;
-      if (!attr) {
-        UTV_CUDA(cudaFuncSetAttribute(qr2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(SMEM_ROWS_MAX * SROW * sizeof(double))));
-        attr = true;
-      }
+      static std::atomic<unsigned long long> attr{0};
+      ensure_smem_attr(qr2_kernel<true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr);
       const size_t smem_bytes = smem ? (size_t)Lr * SROW * sizeof(double) : 0;
       UTV_CUDA(cudaLaunchCooperativeKernel(smem ? (void*)qr2_kernel<true> : (void*)qr2_kernel<false>, dim3(G),
                                            dim3(QR_THREADS), args, smem_bytes, st));

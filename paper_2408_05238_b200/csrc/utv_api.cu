@@ -127,14 +127,23 @@ struct LocalGroup {
 
 struct LocalComm : Comm {
   std::shared_ptr<LocalGroup> g;
+  int device = 0;
   double* tmp = nullptr;
+  double* stage = nullptr;        // a peer's buffer copied to this device (ranks on other GPUs)
   size_t tmp_n = 0;
   void ensure_tmp(size_t n) {
     if (tmp_n >= n) return;
     if (tmp) cudaFree(tmp);
-    tmp = nullptr; tmp_n = 0;
+    if (stage) cudaFree(stage);
+    tmp = stage = nullptr; tmp_n = 0;
     UTV_CUDA(cudaMalloc((void**)&tmp, n * sizeof(double)));
+    UTV_CUDA(cudaMalloc((void**)&stage, n * sizeof(double)));
     tmp_n = n;
+  }
+  bool local(const void* p) const {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice && a.device == device;
   }
   void allreduce(double* buf, size_t n, cudaStream_t st) override {
     if (!n) return;
@@ -143,7 +152,14 @@ struct LocalComm : Comm {
     g->ptr[rank] = buf;
     g->barrier();
     UTV_CUDA(cudaMemcpyAsync(tmp, g->ptr[0], n * sizeof(double), cudaMemcpyDefault, st));
-    for (int r = 1; r < nranks; ++r) launch_axpy(st, (int64_t)n, 1.0, g->ptr[r], tmp);
+    for (int r = 1; r < nranks; ++r) {
+      const double* src = g->ptr[r];
+      if (!local(src)) {                      // kernels read only this device's memory
+        UTV_CUDA(cudaMemcpyAsync(stage, src, n * sizeof(double), cudaMemcpyDefault, st));
+        src = stage;
+      }
+      launch_axpy(st, (int64_t)n, 1.0, src, tmp);
+    }
     UTV_CUDA(cudaStreamSynchronize(st));
     g->barrier();                                            // every rank has read every buffer
     UTV_CUDA(cudaMemcpyAsync(buf, tmp, n * sizeof(double), cudaMemcpyDefault, st));
@@ -172,6 +188,7 @@ struct LocalComm : Comm {
   void abort() override { g->abort(); }
   ~LocalComm() override {
     if (tmp) cudaFree(tmp);
+    if (stage) cudaFree(stage);
   }
 };
 
@@ -1357,6 +1374,7 @@ utv_status utv_create_local_group(utv_handle* handles, int nranks, const int* de
     for (int q = 0; q < nranks; ++q) share += devices[q] == devices[r];
     h->coop_share = std::max(1, share);
     auto* c = new LocalComm();
+    c->device = devices[r];
     c->g = g;
     c->nranks = nranks;
     c->rank = r;
