@@ -773,7 +773,7 @@ struct Ooc {
   double* res = nullptr;  // device, m x (n - c_res), ld m
   int64_t cw = 0;         // staging chunk width (columns, multiple of b)
   double* stg[utv_handle_s::kStg] = {};
-  double* pb = nullptr;   // device m x b: the step's own block column when it is streamed
+  double* pb[2] = {};     // device m x b: a step's own block column when it is streamed (by step parity)
   int next = 0;
 };
 
@@ -830,19 +830,19 @@ void ooc_pass(Ooc& o, const Ctx& c, int64_t c0, int64_t row0, bool write_back, F
 }
 
 // Device pointer (row 0, ld *ld) of the column block [j0, j0 + w), rows 0:rows loaded if streamed.
-double* ooc_block(Ooc& o, const Ctx& c, int64_t j0, int64_t w, int64_t rows, int64_t* ld) {
+double* ooc_block(Ooc& o, const Ctx& c, int64_t j0, int64_t w, int64_t rows, int64_t* ld, int buf = 0) {
   *ld = o.m;
   if (j0 >= o.c_res) return o.res + cm(0, j0 - o.c_res, o.m);
-  UTV_CUDA(cudaEventRecord(o.h->ev_done, c.st));                      // pb's previous readers
+  UTV_CUDA(cudaEventRecord(o.h->ev_done, c.st));                      // the buffer's previous readers
   UTV_CUDA(cudaStreamWaitEvent(o.h->h2d, o.h->ev_done, 0));
   ooc_sync_wb(o);
-  ooc_load(o, c, o.pb, o.m, 0, rows, j0, w, o.h->ev_loaded[0]);
-  return o.pb;
+  ooc_load(o, c, o.pb[buf], o.m, 0, rows, j0, w, o.h->ev_loaded[0]);
+  return o.pb[buf];
 }
 
-void ooc_block_store(Ooc& o, const Ctx& c, int64_t j0, int64_t w) {
+void ooc_block_store(Ooc& o, const Ctx& c, int64_t j0, int64_t w, int buf) {
   if (j0 >= o.c_res) return;
-  ooc_store(o, c, o.pb, o.m, 0, o.m, j0, w, nullptr);
+  ooc_store(o, c, o.pb[buf], o.m, 0, o.m, j0, w, nullptr);
 }
 
 // diag(T) is gathered into dg (n) as each block's sigma is set; C (device, ldc) becomes U^T B.
@@ -866,6 +866,8 @@ void factor_ooc(const Ctx& c, Ooc& o, double* Cd, int64_t ldc, int64_t k, const 
     launch_check_finite(st, m, n - o.c_res, o.res, m, c.h->flag);
   }
   bool y_ready = false;
+  bool fin_pending = false, us_pend = false;        // the previous step's SVD results (see below)
+  int64_t fin_step = 0, fin_j0 = 0, fin_bw = 0;
   for (int64_t j0 = 0, step = 0; j0 < n; j0 += b, ++step) {
     const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0, nr = np - bw;
     const bool right = np > b;                                                     // R5
@@ -897,10 +899,40 @@ void factor_ooc(const Ctx& c, Ooc& o, double* Cd, int64_t ldc, int64_t k, const 
       });
       c.gemm(false, false, m, b, b, 1.0, X, m, Tvs, b, 0.0, X2, m);
     }
-    // ---- block i: right update, panel QR (a5), C := Q_U^T C, SVD and its updates (a7)
+    // ---- block i: right update, the previous step's deferred SVD results, panel QR (a5),
+    // C := Q_U^T C, and this step's SVD launched on the side stream (a7).  The SVD results are
+    // applied one step later (as on the in-core path): A12 := U_s^T A12 commutes with the next
+    // step's right updates, and block i itself is finalised (Sigma, A01 V_s) and written back at
+    // the next step, so the Jacobi overlaps the next step's link-bound passes.
+    const int buf = (int)(step & 1);
     int64_t lda_i = m;
-    double* Ai = ooc_block(o, c, j0, bw, m, &lda_i);
+    double* Ai = ooc_block(o, c, j0, bw, m, &lda_i, buf);
     if (right) c.gemm(false, true, m, bw, b, -1.0, X2, m, WV, np, 1.0, Ai, lda_i);
+    if (fin_pending) {
+      UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
+      const double* Usp = (fin_step & 1) ? c.at(L.Us2) : Us;
+      const double* sgp = (fin_step & 1) ? c.at(L.sig2) : sig;
+      const double* Vsp = fv->Vs + (size_t)fin_step * b * b;
+      // block i's part of A12(i-1): rows fin_j0:fin_j0+fin_bw
+      c.gemm(true, false, fin_bw, bw, fin_bw, 1.0, Usp, b, Ai + fin_j0, lda_i, 0.0, Z1, fin_bw);
+      launch_copy(st, fin_bw, bw, Z1, fin_bw, Ai + fin_j0, lda_i);
+      // finalise block i-1: A11 := Sigma, A01 := A01 V_s, C1 := U_s^T C1, diag(T), write back
+      int64_t ldf = m;
+      double* Af = fin_j0 >= o.c_res ? o.res + cm(0, fin_j0 - o.c_res, m) : o.pb[fin_step & 1];
+      launch_set_diag(st, fin_bw, sgp, Af + fin_j0, ldf);
+      launch_copy(st, fin_bw, 1, sgp, fin_bw, dg + fin_j0, n);
+      if (fin_j0 > 0) {
+        c.gemm(false, false, fin_j0, fin_bw, fin_bw, 1.0, Af, ldf, Vsp, b, 0.0, tmp, fin_j0);
+        launch_copy(st, fin_j0, fin_bw, tmp, fin_j0, Af, ldf);
+      }
+      if (Cd && k > 0) {
+        c.gemm(true, false, fin_bw, k, fin_bw, 1.0, Usp, b, Cd + fin_j0, ldc, 0.0, Z1, fin_bw);
+        launch_copy(st, fin_bw, k, Z1, fin_bw, Cd + fin_j0, ldc);
+      }
+      ooc_block_store(o, c, fin_j0, fin_bw, (int)(fin_step & 1));
+      fin_pending = false;
+      us_pend = nr > 0;                  // rows fin_j0:+fin_bw of the columns > block i: in the U pass
+    }
     panel_qr(st, mp, bw, Ai + j0, lda_i, Wu, m, tauu, Tu, b, c.pw);
     if (Cd && k > 0) {
       double* Cr = Cd + j0;
@@ -908,36 +940,60 @@ void factor_ooc(const Ctx& c, Ooc& o, double* Cd, int64_t ldc, int64_t k, const 
       c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
       c.gemm(false, false, mp, k, bw, -1.0, Wu, m, Z2, bw, 1.0, Cr, ldc);
     }
-    double* Vsi = fv->Vs + (size_t)step * b * b;
-    svd_small(st, bw, Ai + j0, lda_i, Us, b, sig, Vsi, b, c.sw);
-    launch_set_diag(st, bw, sig, Ai + j0, lda_i);
-    launch_copy(st, bw, 1, sig, bw, dg + j0, n);
-    if (j0 > 0) {                                                                  // A01 := A01 V_s
-      c.gemm(false, false, j0, bw, bw, 1.0, Ai, lda_i, Vsi, b, 0.0, tmp, j0);
-      launch_copy(st, j0, bw, tmp, j0, Ai, lda_i);
+    {
+      double* Vsi = fv->Vs + (size_t)step * b * b;
+      double* Usi = buf ? c.at(L.Us2) : Us;
+      double* sgi = buf ? c.at(L.sig2) : sig;
+      UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
+      UTV_CUDA(cudaStreamWaitEvent(c.side, c.h->ev_panel, 0));
+      svd_small(c.side, bw, Ai + j0, lda_i, Usi, b, sgi, Vsi, b, c.sw);
+      UTV_CUDA(cudaEventRecord(c.h->ev_svd, c.side));
     }
-    if (Cd && k > 0) {                                                             // C1 := U_s^T C1
-      c.gemm(true, false, bw, k, bw, 1.0, Us, b, Cd + j0, ldc, 0.0, Z1, bw);
-      launch_copy(st, bw, k, Z1, bw, Cd + j0, ldc);
-    }
-    ooc_block_store(o, c, j0, bw);
     // ---- one read+write pass over the trailing columns (+ the next step's sketch product)
     if (nr > 0) {
       const bool next_sketch = nr > b;
       if (next_sketch) launch_sketch(st, opt.seed, step + 1, j0 + b, mp - b, b, G, mp - b, ns);
+      const bool upd_prev = us_pend;
+      const double* Usp = ((step - 1) & 1) ? c.at(L.Us2) : Us;
+      const int64_t pj0 = j0 - b;
       ooc_pass(o, c, j0 + bw, 0, true, [&](double* d, int64_t ld, int64_t col, int64_t w) {
         if (right) c.gemm(false, true, m, w, b, -1.0, X2, m, WV + (col - j0), np, 1.0, d, ld);
+        if (upd_prev) {                                                            // A12(i-1) := U_s^T A12
+          c.gemm(true, false, b, w, b, 1.0, Usp, b, d + pj0, ld, 0.0, Z1, b);
+          launch_copy(st, b, w, Z1, b, d + pj0, ld);
+        }
         double* dr = d + j0;                                                       // a6, R3
         c.gemm(true, false, bw, w, mp, 1.0, Wu, m, dr, ld, 0.0, Z1, bw);
         c.gemm(true, false, bw, w, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
         c.gemm(false, false, mp, w, bw, -1.0, Wu, m, Z2, bw, 1.0, dr, ld);
-        c.gemm(true, false, bw, w, bw, 1.0, Us, b, dr, ld, 0.0, Z1, bw);          // A12 := U_s^T A12
-        launch_copy(st, bw, w, Z1, bw, dr, ld);
         if (next_sketch)
           c.gemm(true, false, w, b, mp - b, 1.0, d + j0 + b, ld, G, mp - b, 0.0, Y + (col - j0 - b), np - b);
       });
       y_ready = next_sketch;
     }
+    us_pend = false;
+    fin_pending = true;
+    fin_step = step; fin_j0 = j0; fin_bw = bw;
+  }
+  // the last block: its SVD results
+  if (fin_pending) {
+    UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
+    const double* Usp = (fin_step & 1) ? c.at(L.Us2) : Us;
+    const double* sgp = (fin_step & 1) ? c.at(L.sig2) : sig;
+    const double* Vsp = fv->Vs + (size_t)fin_step * b * b;
+    int64_t ldf = m;
+    double* Af = fin_j0 >= o.c_res ? o.res + cm(0, fin_j0 - o.c_res, m) : o.pb[fin_step & 1];
+    launch_set_diag(st, fin_bw, sgp, Af + fin_j0, ldf);
+    launch_copy(st, fin_bw, 1, sgp, fin_bw, dg + fin_j0, n);
+    if (fin_j0 > 0) {
+      c.gemm(false, false, fin_j0, fin_bw, fin_bw, 1.0, Af, ldf, Vsp, b, 0.0, tmp, fin_j0);
+      launch_copy(st, fin_j0, fin_bw, tmp, fin_j0, Af, ldf);
+    }
+    if (Cd && k > 0) {
+      c.gemm(true, false, fin_bw, k, fin_bw, 1.0, Usp, b, Cd + fin_j0, ldc, 0.0, Z1, fin_bw);
+      launch_copy(st, fin_bw, k, Z1, fin_bw, Cd + fin_j0, ldc);
+    }
+    ooc_block_store(o, c, fin_j0, fin_bw, (int)(fin_step & 1));
   }
 }
 
@@ -1013,7 +1069,7 @@ int64_t lstsq_streamed(utv_handle h, int64_t m, int64_t n, int64_t k, double* A,
   }();
   const int64_t cw = std::min<int64_t>(chunk_blocks * b, (n + b - 1) / b * b);
   const size_t kk = (size_t)std::max<int64_t>(k, 1);
-  const size_t fixed = (size_t)m * kk + (size_t)n * kk + (size_t)n + 64 + (size_t)m * b +
+  const size_t fixed = (size_t)m * kk + (size_t)n * kk + (size_t)n + 64 + 2 * (size_t)m * b +
                        (size_t)utv_handle_s::kStg * m * cw;
   size_t free_b = 0, total_b = 0;
   UTV_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -1043,7 +1099,8 @@ int64_t lstsq_streamed(utv_handle h, int64_t m, int64_t n, int64_t k, double* A,
   double* Cd = p; p += (size_t)m * kk;
   double* Xd = p; p += (size_t)n * kk;
   double* dg = p; p += (size_t)n + 64;
-  o.pb = p; p += (size_t)m * b;
+  o.pb[0] = p; p += (size_t)m * b;
+  o.pb[1] = p; p += (size_t)m * b;
   for (int s = 0; s < utv_handle_s::kStg; ++s) { o.stg[s] = p; p += (size_t)m * cw; }
   o.res = p;
   h->ooc_resident_cols = n - o.c_res;
