@@ -123,3 +123,35 @@ def test_streamed_errors(utv, h):
         h.lstsq(Ah, B, X, utv.Opts(block=16, flags=utv.UTV_HOST_STREAMED))
     assert e.value.status == utv.UTV_ERR_ALLOC
     h.set_device_budget(0)
+
+
+def test_streamed_device_budget_limits_residency(utv, monkeypatch):
+    """utv_set_device_budget: with a budget just above the fixed working set (workspace, factored V,
+    staging) part of A stays on the host, and the result is unchanged."""
+    monkeypatch.delenv("UTV_OOC_MAX_RESIDENT_COLS", raising=False)
+    m, n, r, b, q = 4096, 4096, 1800, 256, 1
+    M = gen.GpMatrix(m, n, r, seed=17)
+    B, X0 = M.known_rhs(k=1)
+    hd = utv.Handle(0)                       # fresh handle: no workspace left over from larger calls
+    try:
+        _, _, X_all, r_all = streamed(utv, hd, M.A, B, b, q, 9)
+        assert hd.stream_stats()["resident_cols"] == n
+        done = False
+        for budget in np.arange(0.30e9, 0.60e9, 0.02e9):
+            hd.set_device_budget(int(budget))
+            try:
+                _, _, X_b, r_b = streamed(utv, hd, M.A, B, b, q, 9)
+            except utv.UtvError as e:
+                assert e.status == utv.UTV_ERR_ALLOC
+                continue
+            st_b = hd.stream_stats()
+            if st_b["resident_cols"] == n:
+                break                            # the budget now holds everything: no partial point hit
+            assert r_b == r_all == r
+            assert np.linalg.norm(X_b - X_all) <= 1e-12 * np.linalg.norm(X_all)
+            assert np.linalg.norm(X_b - X0) <= 1e-10 * np.linalg.norm(X0)
+            done = True
+            break
+        assert done, "no budget gave a partially resident run"
+    finally:
+        hd.close()
