@@ -85,6 +85,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   __shared__ double red[NBMAX];
   __shared__ double piv[NBMAX];              // row j: W values (< j) and P values (>= j)
   __shared__ double sw[NBMAX];               // w_l = v^T P[:, l]
+  __shared__ double swz[NBMAX];              // sw, zero for l <= j and l >= nb (SMEM row update)
   __shared__ double ssg[NBMAX];              // s_p = W[:, p]^T v
   __shared__ double sT[NBMAX * NBMAX];
   __shared__ double s_tau, s_beta, s_scal;
@@ -113,6 +114,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   unsigned gen = s_gen;
 
   double acc[NBMAX];
+  double scal_prev = 0.0;                    // SMEM path: scal of the previous column
 #pragma unroll
   for (int v = 0; v < NBMAX; ++v) acc[v] = 0.0;
   for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {        // column 0: rows i > 0
@@ -199,9 +201,13 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     __syncthreads();
     const double tj = s_tau, scal = s_scal, beta = s_beta;
     if (tid < nb) {
-      if (tid > j) sw[tid] = piv[tid] + red[tid] * scal;       // v^T P[:, l], v_j = 1
-      else if (tid < j) ssg[tid] = piv[tid] + red[tid] * scal; // W[:, p]^T v
+      // SMEM path: the previous column's running sums used its pre-scaling values x (the stored
+      // Householder entries are x * scal_prev), so that one partial sum is rescaled here
+      const double rv = (SMEM && tid == j - 1) ? red[tid] * scal_prev : red[tid];
+      if (tid > j) sw[tid] = piv[tid] + rv * scal;            // v^T P[:, l], v_j = 1
+      else if (tid < j) ssg[tid] = piv[tid] + rv * scal;      // W[:, p]^T v
     }
+    if (SMEM && tid < NBMAX) swz[tid] = (tid > j && tid < nb) ? piv[tid] + red[tid] * scal : 0.0;
     __syncthreads();
     if (blockIdx.x == 0) {
       // dlarft: T[0:j, j] = -tau_j T[0:j, 0:j] s ; T[j, j] = tau_j
@@ -216,6 +222,39 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     for (int v = 0; v < NBMAX; ++v) acc[v] = 0.0;
     tr(j, 2);
     const bool next = (j + 1 < nb);
+    if constexpr (SMEM) {
+      // Rows in shared memory: the pivot columns are read and written with a runtime index, and
+      // the reflector is applied to every column with the zero-padded swz (no per-column selects);
+      // column j keeps its pre-scaling value in registers, so acc[j] is rescaled next column.
+      for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
+        if (i < j) continue;
+        double* srow = sp + (i - r0) * SROW;
+        double row[NBMAX];
+#pragma unroll
+        for (int c = 0; c < NBMAX; ++c) row[c] = (c < nb) ? srow[c] : 0.0;
+        const double xj = srow[j];
+        const double xj1 = next ? srow[j + 1] : 0.0;
+        const double swj1 = next ? swz[j + 1] : 0.0;
+        const double v = (i == j) ? 1.0 : xj * scal;
+        const double newj = (i == j) ? beta : v;
+        const double tv = tj * v;
+        const bool acc_next = next && i > j + 1;
+        const double xn = xj1 - tv * swj1;
+#pragma unroll
+        for (int c = 0; c < NBMAX; ++c) row[c] -= tv * swz[c];
+#pragma unroll
+        for (int c = 0; c < NBMAX; ++c)
+          if (c < nb) srow[c] = row[c];
+        srow[j] = newj;
+        if (acc_next) {
+#pragma unroll
+          for (int c = 0; c < NBMAX; ++c) acc[c] += xn * row[c];
+        }
+      }
+      scal_prev = scal;
+      __syncthreads();
+      continue;
+    }
     for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
       if (i < j) continue;                   // rows above the pivot: untouched
       // load the whole row first (all loads in flight; no shared-memory store in between that the
