@@ -88,7 +88,6 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   __shared__ double swz[NBMAX];              // sw, zero for l <= j and l >= nb (SMEM row update)
   __shared__ double ssg[NBMAX];              // s_p = W[:, p]^T v
   __shared__ double sT[NBMAX * NBMAX];
-  __shared__ double s_tau, s_beta, s_scal;
   __shared__ unsigned s_gen;
 
   const unsigned G = gridDim.x;
@@ -185,21 +184,20 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       __syncthreads();
     }
     tr(j, 1);
-    if (tid == 0) {                          // dlarfg on x = P[j:, j]
+    // dlarfg on x = P[j:, j], evaluated redundantly by every thread (identical inputs and
+    // operations, so identical results) instead of by thread 0 plus a broadcast barrier
+    double tj, beta, scal;
+    {
       const double alpha = piv[j];
       const double xi = sqrt(red[j]);
-      double t, beta, scal;
       if (xi == 0.0) {
-        t = 0.0; beta = alpha; scal = 0.0;
+        tj = 0.0; beta = alpha; scal = 0.0;
       } else {
         beta = -copysign(hypot(alpha, xi), alpha);
-        t = (beta - alpha) / beta;
+        tj = (beta - alpha) / beta;
         scal = 1.0 / (alpha - beta);
       }
-      s_tau = t; s_beta = beta; s_scal = scal;
     }
-    __syncthreads();
-    const double tj = s_tau, scal = s_scal, beta = s_beta;
     if (tid < nb) {
       // SMEM path: the previous column's running sums used its pre-scaling values x (the stored
       // Householder entries are x * scal_prev), so that one partial sum is rescaled here
