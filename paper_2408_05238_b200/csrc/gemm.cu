@@ -66,15 +66,20 @@ constexpr int tile_doubles() { return MN_MAJOR ? BK * (BMN + 8) : BMN * LD_K; }
 //      overlaps the other's main loop)
 //   2: 128 x 128, 4 x 2 warps of 32 x 64, 256 threads, 1 CTA / SM
 //   3:  64 x 128, 2 x 2 warps of 32 x 64, 128 threads, 2 CTAs / SM
+//   4: 128 x  32, 4 x 1 warps of 32 x 32, 128 threads, 3 CTAs / SM  (N <= 32: the panel's
+//      P_r^T W products and the few-RHS updates, which would waste most of a 64/128-wide tile)
 template <int ID> struct Shape;
 template <> struct Shape<0> { static constexpr int BM = 128, WM = 2, WN = 4, MI = 4, NJ = 4, CTAS = 1; };
 template <> struct Shape<1> { static constexpr int BM = 128, WM = 2, WN = 2, MI = 4, NJ = 4, CTAS = 2; };
 template <> struct Shape<2> { static constexpr int BM = 128, WM = 4, WN = 2, MI = 2, NJ = 8, CTAS = 1; };
 template <> struct Shape<3> { static constexpr int BM = 64, WM = 2, WN = 2, MI = 2, NJ = 8, CTAS = 2; };
-constexpr int kNumShapes = 4;
+template <> struct Shape<4> { static constexpr int BM = 128, WM = 4, WN = 1, MI = 2, NJ = 4, CTAS = 3; };
+constexpr int kNumShapes = 5;
+constexpr int kNarrowCfg = 4;
 __host__ __device__ constexpr int shape_bm(int id) { return id == 3 ? 64 : 128; }
-__host__ __device__ constexpr int shape_bn(int id) { return id == 1 ? 64 : 128; }
-__host__ __device__ constexpr int shape_ctas(int id) { return (id == 1 || id == 3) ? 2 : 1; }
+__host__ __device__ constexpr int shape_bn(int id) { return id == 1 ? 64 : (id == 4 ? 32 : 128); }
+__host__ __device__ constexpr int shape_ctas(int id) { return id == 4 ? 3 : ((id == 1 || id == 3) ? 2 : 1); }
+__host__ __device__ constexpr int smem_budget_kb(int ctas) { return ctas == 1 ? 200 : (ctas == 2 ? 108 : 72); }
 
 template <bool TA, bool TB, int ID>
 struct Cfg {
@@ -89,7 +94,7 @@ struct Cfg {
   static constexpr int B_DBL = tile_doubles<BN, B_MN>();
   static constexpr int STAGE_DBL = A_DBL + B_DBL;
   static constexpr int CTAS_PER_SM = Shape<ID>::CTAS;
-  static constexpr int SMEM_BUDGET = (CTAS_PER_SM == 1 ? 200 : 110) * 1024;
+  static constexpr int SMEM_BUDGET = smem_budget_kb(CTAS_PER_SM) * 1024;
   static constexpr int STAGES_FIT = SMEM_BUDGET / (STAGE_DBL * 8);
   static constexpr int STAGES = STAGES_FIT > 4 ? 4 : STAGES_FIT;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_DBL * sizeof(double);
@@ -359,7 +364,7 @@ struct TmaCfg {
   static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int CTAS_PER_SM = Shape<ID>::CTAS;
-  static constexpr int SMEM_BUDGET = (CTAS_PER_SM == 1 ? 210 : 108) * 1024;
+  static constexpr int SMEM_BUDGET = (CTAS_PER_SM == 1 ? 210 : smem_budget_kb(CTAS_PER_SM)) * 1024;
   static constexpr int STAGES_FIT = SMEM_BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024;   // + alignment slack
@@ -674,7 +679,7 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int num_sms, size_t work_
     return true;
   }();
   (void)env_read;
-  const int cfg = g_force_wn ? g_force_wn : (K <= 1024 ? g_cfg_short : g_cfg_long);
+  const int cfg = g_force_wn ? g_force_wn : (N <= 32 ? kNarrowCfg : (K <= 1024 ? g_cfg_short : g_cfg_long));
   const int bm = shape_bm(cfg), bn = shape_bn(cfg), ctas = shape_ctas(cfg);
   Plan best{cfg, 1, K};
   double best_t = 1e300;
@@ -734,18 +739,28 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
       case 0: done = dispatch_tma<0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
       case 1: done = dispatch_tma<1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
       case 2: done = dispatch_tma<2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-      default: done = dispatch_tma<3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+      case 3: done = dispatch_tma<3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+      default: done = dispatch_tma<4>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
     }
   }
-  if (!done) switch (plan.cfg | (aligned ? 0 : 4)) {
-    case 0: dispatch<2, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    case 1: dispatch<2, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    case 2: dispatch<2, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    case 3: dispatch<2, 3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    case 4: dispatch<1, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    case 5: dispatch<1, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    case 6: dispatch<1, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-    default: dispatch<1, 3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+  if (!done) {                     // cp.async fallback: the narrow tile runs as 128 x 64 there
+    if (aligned) {
+      switch (plan.cfg) {
+        case 0: dispatch<2, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        case 1: dispatch<2, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        case 2: dispatch<2, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        case 3: dispatch<2, 3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        default: dispatch<2, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+      }
+    } else {
+      switch (plan.cfg) {
+        case 0: dispatch<1, 0>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        case 1: dispatch<1, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        case 2: dispatch<1, 2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        case 3: dispatch<1, 3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+        default: dispatch<1, 1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+      }
+    }
   }
   if (splits > 1) {
     const int64_t total = M * N;

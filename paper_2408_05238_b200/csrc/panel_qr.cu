@@ -338,12 +338,13 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
     const int64_t wr = w - jb - nb;
     if (wr > 0) {
       double* Pr = P + cm(jb, jb + nb, ldp);
-      // Z1 = W_b^T P_r ; Z2 = T_b^T Z1 ; P_r -= W_b Z2      (apply Q_b^T from the left)
-      dgemm(st, true, false, nb, wr, R, 1.0, Wb, ldw, Pr, ldp, 0.0, pw.z1, nb, pw.gemm_work, pw.gemm_work_doubles,
+      // Apply Q_b^T from the left, transposed so the skinny dimension (nb <= 32) is the GEMMs' N
+      // (the narrow 128 x 32 tile): Z1^T = P_r^T W_b ; Z2^T = Z1^T T_b ; P_r -= W_b (Z2^T)^T
+      dgemm(st, true, false, wr, nb, R, 1.0, Pr, ldp, Wb, ldw, 0.0, pw.z1, wr, pw.gemm_work, pw.gemm_work_doubles,
             pw.num_sms);
-      dgemm(st, true, false, nb, wr, nb, 1.0, Tb, ldt, pw.z1, nb, 0.0, pw.z2, nb, pw.gemm_work,
+      dgemm(st, false, false, wr, nb, nb, 1.0, pw.z1, wr, Tb, ldt, 0.0, pw.z2, wr, pw.gemm_work,
             pw.gemm_work_doubles, pw.num_sms);
-      dgemm(st, false, false, R, wr, nb, -1.0, Wb, ldw, pw.z2, nb, 1.0, Pr, ldp, pw.gemm_work,
+      dgemm(st, false, true, R, wr, nb, -1.0, Wb, ldw, pw.z2, wr, 1.0, Pr, ldp, pw.gemm_work,
             pw.gemm_work_doubles, pw.num_sms);
     }
   }

@@ -44,6 +44,10 @@ for n in [int(a) for a in sys.argv[1:]] or (20000, 19744):
     check("update NT K=512", False, True, n, n, 512, beta=1.0)
     check("update NT K=256", False, True, n, n, 256, beta=1.0)
     check("update NN K=256", False, False, n, n, 256, beta=1.0)
+check("narrow TN (P_r^T W)", True, False, 224, 32, 50000)
+check("narrow NN", False, False, 20000, 32, 256, beta=1.0)
+check("narrow NT k=1", False, True, 20000, 1, 256, beta=1.0)
+check("narrow TN k=16", True, False, 256, 16, 20000)
 check("sub-view NT", False, True, 7000, 6000, 512, beta=1.0, pad=256, off=256)
 check("sub-view TN", True, False, 6000, 256, 7000, pad=256, off=256)
 check("sub-view NN", False, False, 6000, 256, 7000, beta=1.0, pad=2, off=2)
