@@ -693,6 +693,9 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int num_sms, size_t work_
     const double waves = std::ceil(tiles * sp / slots);
     double t = waves * (2.0 * bm * bn * (double)kc / rate + 2.5e-6);
     if (sp > 1) t += 8.0 * (double)M * (double)N * (sp + 1) / 5.0e12 + 4e-6;
+    // measured (profiles/r01_timeline): unsplit long-K launches run 1-6% below the split ones
+    // of the same size even when their wave count is whole (one CTA streaming all of K)
+    if (sp == 1 && K > 2048) t *= 1.05;
     if (t < best_t * 0.995) { best_t = t; best = Plan{cfg, sp, kc}; }
   }
   return best;
