@@ -68,7 +68,8 @@ def test_sketch_matches_oracle(h, seed, step, row0, mrows, b):
 
 # ----------------------------------------------------------------------------- GEMM primitive
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
-@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (130, 67, 33), (257, 129, 300), (64, 256, 5000)])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (130, 67, 33), (257, 129, 300), (64, 256, 5000),
+                                   (300, 17, 5000), (5000, 32, 300), (1000, 1, 2000)])   # N <= 32: narrow tile
 def test_gemm_vs_numpy(h, ta, tb, M, N, K):
     rng = np.random.default_rng(M * N + K)
     A = rng.standard_normal((K, M) if ta else (M, K))
