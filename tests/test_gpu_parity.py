@@ -300,3 +300,28 @@ def test_factored_v_equals_explicit_v(utv, m, n, r, b, q):
     Xe = host(Xe)
     assert rf == re
     assert np.linalg.norm(Xf - Xe) <= 1e-12 * np.linalg.norm(Xe)
+
+
+# ----------------------------------------------------------------------------- randomized sweep
+def _random_cases(count=16, seed=20241017):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        n = int(rng.integers(40, 700))
+        m = n + int(rng.integers(0, 400))
+        b = int(rng.choice([8, 16, 32, 48, 64, 100, 128, 256]))
+        r = int(rng.integers(1, n + 1))
+        out.append((m, n, r, b, int(rng.integers(0, 3)), int(rng.integers(1, 5))))
+    return out
+
+
+@pytest.mark.parametrize("m,n,r,b,q,k", _random_cases())
+def test_lstsq_random_shapes(utv, m, n, r, b, q, k):
+    """Seeded random shapes (b not dividing n, tall, rank inside a block, several RHS): r identical,
+    x within 1e-9 of the oracle."""
+    M = gen.GpMatrix(m, n, r, seed=m * 7 + n)
+    B, _ = M.known_rhs(k=k, consistent=m < 2 * r)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=13)
+    Xg, rg = _lstsq_gpu(utv, M.A, B, b, q, seed=13)
+    assert rg == ro
+    assert np.linalg.norm(Xg - Xo) <= 1e-9 * max(np.linalg.norm(Xo), 1e-300)
