@@ -171,3 +171,28 @@ def test_local_group_failing_rank_releases_peers(utv):
     finally:
         for h in hs:
             h.close()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_local_group_random_shapes(utv, seed):
+    """Seeded random shapes and rank counts through the in-process multi-rank path vs the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    P = int(rng.integers(2, 5))
+    n = int(rng.integers(60, 500))
+    m = n + int(rng.integers(0, 300))
+    b = int(rng.choice([16, 32, 64, 128]))
+    r = int(rng.integers(1, n + 1))
+    q = int(rng.integers(0, 3))
+    k = int(rng.integers(1, 3))
+    M = gen.GpMatrix(m, n, r, seed=seed * 17 + n)
+    B, _ = M.known_rhs(k=k, consistent=m < 2 * r)
+    B = B.reshape(m, -1)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=seed)
+    hs = utv.local_group(P)
+    try:
+        Xs, rs = run_group(utv, hs, M.A, B, b, q, seed)
+    finally:
+        for hh in hs:
+            hh.close()
+    assert all(x == ro for x in rs), (rs, ro)
+    assert np.linalg.norm(Xs[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)

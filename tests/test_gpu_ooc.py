@@ -155,3 +155,23 @@ def test_streamed_device_budget_limits_residency(utv, monkeypatch):
         assert done, "no budget gave a partially resident run"
     finally:
         hd.close()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_streamed_random_shapes(utv, h, monkeypatch, seed):
+    """Seeded random shapes and resident caps through the out-of-core mode vs the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(60, 600))
+    m = n + int(rng.integers(0, 300))
+    b = int(rng.choice([16, 32, 64, 96, 128]))
+    r = int(rng.integers(1, n + 1))
+    q = int(rng.integers(0, 3))
+    k = int(rng.integers(1, 4))
+    cap = int(rng.integers(0, n + b))
+    monkeypatch.setenv("UTV_OOC_MAX_RESIDENT_COLS", str(cap))
+    M = gen.GpMatrix(m, n, r, seed=seed * 31 + n)
+    B, _ = M.known_rhs(k=k, consistent=m < 2 * r)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=seed)
+    _, _, Xg, rg = streamed(utv, h, M.A, B, b, q, seed)
+    assert rg == ro
+    assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
