@@ -279,7 +279,8 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    h.profile(True)
+    if not args.no_profile:
+        h.profile(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -501,6 +502,8 @@ def main():
     ap.add_argument("--ref-n", type=int, default=1536)
     ap.add_argument("--force-dist", action="store_true", help="use the multi-GPU (block-cyclic) path even at N=1")
     ap.add_argument("--profile-dump", default="", help="write every timed launch record as CSV (diagnostics)")
+    ap.add_argument("--no-profile", action="store_true",
+                    help="diagnostics: no per-launch events in the timed step (roofline fields then empty)")
     ap.add_argument("--streamed", type=int, default=-1,
                     help="out-of-core mode: keep at most this many columns of A resident in HBM")
     args = ap.parse_args()
