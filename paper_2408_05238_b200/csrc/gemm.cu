@@ -68,17 +68,21 @@ constexpr int tile_doubles() { return MN_MAJOR ? BK * (BMN + 8) : BMN * LD_K; }
 //   3:  64 x 128, 2 x 2 warps of 32 x 64, 128 threads, 2 CTAs / SM
 //   4: 128 x  32, 4 x 1 warps of 32 x 32, 128 threads, 3 CTAs / SM  (N <= 32: the panel's
 //      P_r^T W products and the few-RHS updates, which would waste most of a 64/128-wide tile)
+//   5:  64 x  64, 2 x 2 warps of 32 x 32, 128 threads, 3 CTAs / SM  (short K, the default: with 12
+//      warps per SM two CTAs keep the DMMA pipe busy through the third one's epilogue; K = 512
+//      update 34.1 -> 34.6 TF/s, K = 256 32.8 -> 33.8 vs config 1; 4 CTAs / SM was worse)
 template <int ID> struct Shape;
 template <> struct Shape<0> { static constexpr int BM = 128, WM = 2, WN = 4, MI = 4, NJ = 4, CTAS = 1; };
 template <> struct Shape<1> { static constexpr int BM = 128, WM = 2, WN = 2, MI = 4, NJ = 4, CTAS = 2; };
 template <> struct Shape<2> { static constexpr int BM = 128, WM = 4, WN = 2, MI = 2, NJ = 8, CTAS = 1; };
 template <> struct Shape<3> { static constexpr int BM = 64, WM = 2, WN = 2, MI = 2, NJ = 8, CTAS = 2; };
 template <> struct Shape<4> { static constexpr int BM = 128, WM = 4, WN = 1, MI = 2, NJ = 4, CTAS = 3; };
-constexpr int kNumShapes = 5;
+template <> struct Shape<5> { static constexpr int BM = 64, WM = 2, WN = 2, MI = 2, NJ = 4, CTAS = 3; };
+constexpr int kNumShapes = 6;
 constexpr int kNarrowCfg = 4;
-__host__ __device__ constexpr int shape_bm(int id) { return id == 3 ? 64 : 128; }
-__host__ __device__ constexpr int shape_bn(int id) { return id == 1 ? 64 : (id == 4 ? 32 : 128); }
-__host__ __device__ constexpr int shape_ctas(int id) { return id == 4 ? 3 : ((id == 1 || id == 3) ? 2 : 1); }
+__host__ __device__ constexpr int shape_bm(int id) { return (id == 3 || id == 5) ? 64 : 128; }
+__host__ __device__ constexpr int shape_bn(int id) { return (id == 1 || id == 5) ? 64 : (id == 4 ? 32 : 128); }
+__host__ __device__ constexpr int shape_ctas(int id) { return (id == 4 || id == 5) ? 3 : ((id == 1 || id == 3) ? 2 : 1); }
 __host__ __device__ constexpr int smem_budget_kb(int ctas) { return ctas == 1 ? 200 : (ctas == 2 ? 108 : 72); }
 
 template <bool TA, bool TB, int ID>
@@ -670,7 +674,7 @@ void dgemm_force_tile_width(int cfg) { g_force_wn = cfg; }
 // SMs is 5.28 waves -> 6 (88%); split 3 gives 2346 tiles = 15.85 -> 16 waves (99%).
 struct Plan { int cfg; int splits; int64_t kc; };
 
-int g_cfg_long = 0, g_cfg_short = 1;     // defaults (overridable: UTV_GEMM_CFG_LONG / _SHORT)
+int g_cfg_long = 0, g_cfg_short = 5;     // defaults (overridable: UTV_GEMM_CFG_LONG / _SHORT)
 
 static Plan make_plan(int64_t M, int64_t N, int64_t K, int num_sms, size_t work_doubles) {
   static const bool env_read = [] {
@@ -743,7 +747,8 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
       case 1: done = dispatch_tma<1>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
       case 2: done = dispatch_tma<2>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
       case 3: done = dispatch_tma<3>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
-      default: done = dispatch_tma<4>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+      case 4: done = dispatch_tma<4>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
+      default: done = dispatch_tma<5>(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial); break;
     }
   }
   if (!done) {                     // cp.async fallback: the narrow tile runs as 128 x 64 there
