@@ -1363,7 +1363,10 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
     UTV_CUDA(cudaMemset(h->bar2, 0, kGridBarrierBytes));
     int lo = 0, hi = 0;
     UTV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    UTV_CUDA(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
+    // The SVD's results are needed only a step later (deferred A12 / finalisation), so its stream
+    // yields SMs to the critical-path GEMMs (measured: cfg3 25.27 -> 25.22 s vs high priority).
+    static const bool side_high = [] { const char* e = std::getenv("UTV_SIDE_HIGH_PRIORITY"); return e && e[0] == '1'; }();
+    UTV_CUDA(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, side_high ? hi : lo));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_panel, cudaEventDisableTiming));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_svd, cudaEventDisableTiming));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_us, cudaEventDisableTiming));
