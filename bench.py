@@ -407,6 +407,9 @@ def run_ours(args):
                                            "products and the side stream (concurrent, so its event times "
                                            "include waiting for SMs)"}},
         "phases_ms_per_step": {k2: v["ms"] / args.steps for k2, v in prof.items()},
+        "phases_note": "sums of event-bracketed launch times per kernel family over all streams; the SVD "
+                       "runs on a low-priority side stream overlapping the main stream, so its times include "
+                       "waiting for SMs (profiles/r01_timeline_cfg3_summary.txt has the critical path)",
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk,
