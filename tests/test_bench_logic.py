@@ -1,0 +1,53 @@
+"""bench.py host logic (CPU): the fixed workload measure F_alg of SURVEY App. B, the factored-V flop
+accounting, and the critical-path GEMM selection used for the roofline."""
+import importlib.util
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def bench():
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_f_alg_matches_survey_cfg3(bench):
+    """F_alg(cfg3) = 1.094e15 (about 26/3 n^3 for square n, q = 2)."""
+    m, n, rank, b, q, k = bench.CONFIGS["cfg3"]
+    F = bench.f_alg(m, n, b, q, k, rank)
+    assert abs(F - 1.094e15) / 1.094e15 < 2e-3
+    assert abs(F - 26.0 / 3.0 * n ** 3) / F < 0.01
+
+
+@pytest.mark.parametrize("q,coef", [(0, 6.0), (1, 22.0 / 3.0), (2, 26.0 / 3.0)])
+def test_f_alg_leading_order_square(bench, q, coef):
+    """Square leading order ((18 + 4q)/3) n^3; b << n so lower-order terms are small."""
+    n, b = 8192, 64
+    F = bench.f_alg(n, n, b, q, 1, n // 2)
+    assert abs(F - coef * n ** 3) / F < 0.02
+
+
+def test_factored_v_accounting(bench):
+    """The explicit-V term is 4 n sum n'b over sketched steps (~2 n^3); the factored apply is tiny."""
+    n, b, k = 4096, 256, 1
+    v = bench.v_accum_flops(n, n, b)
+    assert abs(v - 2.0 * n ** 3) / v < 0.1
+    assert bench.factored_apply_flops(n, b, k, n // 2) < 1e-3 * v
+
+
+def test_big_gemm_selection(bench, tmp_path):
+    """The roofline kernel = GEMM launches (family 0) of >= 4 GFLOP on the first (main) stream."""
+    p = tmp_path / "prof.csv"
+    p.write_text("family,launches,ms,flops,M,N,K,tag,start_ms,stream\n"
+                 "0,1,10.0,3.5e11,50000,256,50000,0,0.0,0\n"       # big, main
+                 "0,1,1.0,1.0e9,256,256,256,0,10.0,0\n"           # small, main
+                 "0,1,5.0,1.0e11,50000,256,50000,0,10.0,7f00\n"   # big, side stream
+                 "1,1,2.0,0.0,0,0,0,0,11.0,0\n")                  # panel
+    st = bench.big_gemm_stats(str(p))
+    assert st["launches"] == 1
+    assert abs(st["tflops"] - 3.5e11 / 10e-3 / 1e12) < 1e-9
