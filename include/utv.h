@@ -65,7 +65,8 @@ utv_status utv_create(utv_handle* handle, int device, void* stream);
  * Multi-GPU handles: one rank per GPU, 1D block-cyclic columns (block n_b = opts->block,
  * block j on rank j mod P).  With such a handle utv_lstsq takes A = THIS RANK's shard: its column
  * blocks packed in order (m x utv_dist_local_cols(n, n_b, P, rank), lda >= m, device memory) and
- * n = the GLOBAL column count; B (m x k, device) is replicated on every rank and overwritten by
+ * n = the GLOBAL column count (the shard is overwritten by this rank's column blocks of T, with
+ * Sigma on the diagonal blocks it owns); B (m x k, device) is replicated on every rank and overwritten by
  * U^T B; X (n x k, device) is written, identical on every rank; *rank is identical on every rank.
  * All ranks must make the same calls with the same m, n, k, opts (collectives in lock step).
  * Fast option with factored V only (UTV_NULLIFY_T12 / UTV_EXPLICIT_V / UTV_HOST_STREAMED ->
