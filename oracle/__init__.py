@@ -157,8 +157,14 @@ def nullify(T, V, r: int):
 
 
 def lstsq(A, B, b: int, q: int, tau: float = 1e-10, seed: int = 1, nullify: bool = False):
-    """randUTV least squares (fig:alg_axb; fast option without Nullify unless nullify=True). Returns (X, r)."""
+    """randUTV least squares (fig:alg_axb; fast option without Nullify unless nullify=True). Returns (X, r).
+
+    m < n goes through lstsq_wide (reading R21)."""
     A = _f64(A); m, n = A.shape
+    if m < n:
+        if nullify:
+            raise OracleError(ERR_ARG)
+        return lstsq_wide(A, B, b, q, tau, seed)
     B2 = _f64(np.asarray(B).reshape(m, -1)); k = B2.shape[1]
     X = np.zeros((n, k), order="F")
     r = C.c_int64(0)
@@ -167,3 +173,27 @@ def lstsq(A, B, b: int, q: int, tau: float = 1e-10, seed: int = 1, nullify: bool
     if st != OK:
         raise OracleError(st)
     return X, int(r.value)
+
+
+def lstsq_wide(A, B, b: int, q: int, tau: float = 1e-10, seed: int = 1):
+    """Wide least squares, m < n (reading R21 in DESIGN.md).
+
+    The paper defines randUTV for m >= n only (its loop guard is garbled, R4).  For m < n the
+    oracle runs randUTV on the tall A^T (n x m): A^T V' = U' T' (eq:UTVdef P:467-473), so
+    A = V' T'^T U'^T, and with r from Compute_rank on T' (R10) the solution of
+    eq:simplesoln transposes to
+        X = U'(:, 0:r) T'(0:r, 0:r)^{-T} V'(:, 0:r)^T B.
+    Steps: the C randUTV (explicit U' and V'), then numpy / scipy library primitives.
+    """
+    from scipy.linalg import solve_triangular
+    A = _f64(A); m, n = A.shape
+    assert m < n
+    B2 = _f64(np.asarray(B).reshape(m, -1)); k = B2.shape[1]
+    f = randutv(np.asfortranarray(A.T), b, q, seed, want_u=True)
+    T, V, U = f["T"], f["V"], f["U"]
+    r = rank(T, tau)
+    if r == 0:
+        return np.zeros((n, k), order="F"), 0
+    c = V[:, :r].T @ B2                                       # V'(:, 0:r)^T B
+    z = solve_triangular(T[:r, :r], c, trans="T", lower=False)  # T11^{-T} c
+    return np.asfortranarray(U[:, :r] @ z), r

@@ -266,6 +266,38 @@ def test_lstsq_full_rank_square_and_tall():
     assert np.linalg.norm(X.ravel() - np.linalg.solve(Ra, Qa.T @ bvec)) <= 1e-12 * np.linalg.norm(X)
 
 
+@pytest.mark.parametrize("m,n,r,b,q", [(20, 30, 8, 4, 1), (30, 64, 30, 16, 2), (11, 40, 5, 3, 0),
+                                       (33, 50, 17, 8, 2), (1, 7, 1, 4, 1), (48, 49, 20, 16, 0)])
+def test_lstsq_wide_matches_pinv_exact_rank(m, n, r, b, q):
+    """R21 (m < n via randUTV of A^T): the min-norm solution on exact-rank inputs (brute-force pinv)."""
+    Gd = gen.GdMatrix(m, n, r, alpha=1.0, seed=m * n + r)
+    B, X0 = Gd.known_rhs(k=2, consistent=r == m)
+    X, rk = oracle.lstsq(Gd.A, B, b=b, q=q, tau=1e-10, seed=5)
+    assert X.shape == (n, 2) and rk == r
+    Xp = _pinv_solution(Gd.A, B, 1e-10)
+    assert np.linalg.norm(X - Xp) <= 1e-11 * np.linalg.norm(Xp)
+    assert np.linalg.norm(X - X0) <= 1e-11 * np.linalg.norm(X0)
+
+
+def test_lstsq_wide_full_row_rank_closed_form():
+    """Full row rank: x = A^T (A A^T)^{-1} b, the textbook minimum-norm solution."""
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((25, 60))
+    bvec = rng.standard_normal(25)
+    X, r = oracle.lstsq(A, bvec, b=8, q=1)
+    assert r == 25
+    xc = A.T @ np.linalg.solve(A @ A.T, bvec)
+    assert np.linalg.norm(X.ravel() - xc) <= 1e-12 * np.linalg.norm(xc)
+    assert np.linalg.norm(A @ X.ravel() - bvec) <= 1e-12 * np.linalg.norm(bvec)
+
+
+def test_lstsq_wide_zero_and_nullify_rejected():
+    X, r = oracle.lstsq(np.zeros((4, 9)), np.ones(4), b=2, q=1)
+    assert r == 0 and X.shape == (9, 1) and not X.any()
+    with pytest.raises(oracle.OracleError):
+        oracle.lstsq(np.ones((3, 5)), np.ones(3), b=2, q=1, nullify=True)
+
+
 def test_rank_edge_cases():
     X, r = oracle.lstsq(np.zeros((10, 6)), np.ones(10), b=4, q=1)
     assert r == 0 and np.all(X == 0.0)
