@@ -32,7 +32,8 @@ typedef struct utv_handle_s* utv_handle;
 typedef enum {
   UTV_OK = 0,
   UTV_ERR_ARG = -1,          /* bad argument (null pointer, ld < rows, b < 1, q < 0, tau not in [0,1)) */
-  UTV_ERR_SHAPE = -2,        /* m < n (the paper's loop guard for wide matrices is garbled: R4) */
+  UTV_ERR_SHAPE = -2,        /* m < n where unsupported: utv_factor / utv_solve (the paper's loop
+                                guard for wide matrices is garbled: R4), multi-GPU or out-of-core lstsq */
   UTV_ERR_ALLOC = -3,        /* device / pinned allocation failed */
   UTV_ERR_CUDA = -4,         /* a CUDA runtime call failed */
   UTV_ERR_NCCL = -5,         /* reserved: multi-GPU communication failure */
@@ -147,6 +148,10 @@ utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const d
  * factored V then also keeps the nullify reflectors, about r (n - r) more doubles).  A, B and X may be HOST pointers (pageable or pinned): they are then staged
  * through device buffers inside the call (the end-to-end path); host A and B are inputs only
  * (left unchanged), a host X is written and the call returns after X has landed.
+ * Wide A (m < n, reading R21): randUTV of the tall A^T (A^T V' = U' T') with
+ * explicit U' and V' (n^2 + m^2 doubles of workspace) and X = U'(:, 0:r) T'11^{-T} V'(:, 0:r)^T B;
+ * A and B are left unchanged; single-GPU in-core only (multi-GPU / UTV_HOST_STREAMED ->
+ * UTV_ERR_SHAPE, UTV_NULLIFY_T12 -> UTV_ERR_UNSUPPORTED).
  */
 utv_status utv_lstsq(utv_handle handle, int64_t m, int64_t n, int64_t k, double* A, int64_t lda,
                      double* B, int64_t ldb, double* X, int64_t ldx, const utv_opts* opts,

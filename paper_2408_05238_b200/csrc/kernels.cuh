@@ -75,5 +75,11 @@ void launch_rz_build(cudaStream_t st, int64_t bw, int64_t nz, const double* T, i
 void launch_rz_writeback(cudaStream_t st, int64_t bw, int64_t nz, const double* M, int64_t ldm, double* T,
                          int64_t ldt, int64_t i0, int64_t r);
 void launch_reverse_rows(cudaStream_t st, int64_t bw, const double* src, int64_t lds, double* dst, int64_t ldd);
+// Wide least squares (R21): dst (cols x rows) = src^T; permutations (mode 0 rows reversed, 1 columns
+// reversed, 2 J src^T J upper triangle of a square upper-triangular src).
+void launch_transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+                      int64_t ldd);
+void launch_permute(cudaStream_t st, int mode, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+                    int64_t ldd);
 
 }  // namespace utv

@@ -206,3 +206,56 @@ void launch_reverse_rows(cudaStream_t st, int64_t bw, const double* src, int64_t
   UTV_CUDA(cudaGetLastError());
 }
 }  // namespace utv
+
+// ---- Wide least squares (m < n, reading R21) ------------------------------
+// A^T through a 32 x 33 shared-memory tile: coalesced column reads of A and column writes of A^T.
+namespace utv {
+namespace {
+constexpr int kTr = 32;
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ src, int64_t lds,
+                                 double* __restrict__ dst, int64_t ldd) {
+  __shared__ double tile[kTr][kTr + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * kTr, c0 = (int64_t)blockIdx.y * kTr;
+  for (int j = threadIdx.y; j < kTr; j += blockDim.y) {               // src column c0 + j
+    const int64_t r = r0 + threadIdx.x, c = c0 + j;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = src[cm(r, c, lds)];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < kTr; j += blockDim.y) {               // dst column r0 + j = src row r0 + j
+    const int64_t dr = c0 + threadIdx.x, dc = r0 + j;
+    if (dr < cols && dc < rows) dst[cm(dr, dc, ldd)] = tile[threadIdx.x][j];
+  }
+}
+// mode 0: dst = J src (rows reversed); mode 1: dst = src J (columns reversed);
+// mode 2 (square, rows == cols): dst = J src^T J restricted to its upper triangle (0 below), i.e.
+// the upper-triangular form of the lower-triangular src^T when src is upper triangular.
+__global__ void permute_kernel(int mode, int64_t rows, int64_t cols, const double* __restrict__ src, int64_t lds,
+                               double* __restrict__ dst, int64_t ldd) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % rows, j = e / rows;
+    double v;
+    if (mode == 0) v = src[cm(rows - 1 - i, j, lds)];
+    else if (mode == 1) v = src[cm(i, cols - 1 - j, lds)];
+    else v = i <= j ? src[cm(rows - 1 - j, rows - 1 - i, lds)] : 0.0;
+    dst[cm(i, j, ldd)] = v;
+  }
+}
+}  // namespace
+
+void launch_transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+                      int64_t ldd) {
+  if (rows * cols <= 0) return;
+  ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)(rows * cols));
+  const dim3 grid((unsigned)((rows + kTr - 1) / kTr), (unsigned)((cols + kTr - 1) / kTr));
+  transpose_kernel<<<grid, dim3(kTr, 8), 0, st>>>(rows, cols, src, lds, dst, ldd);
+  UTV_CUDA(cudaGetLastError());
+}
+void launch_permute(cudaStream_t st, int mode, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+                    int64_t ldd) {
+  if (rows * cols <= 0) return;
+  ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)(rows * cols));
+  permute_kernel<<<grid_for2(rows * cols), 256, 0, st>>>(mode, rows, cols, src, lds, dst, ldd);
+  UTV_CUDA(cudaGetLastError());
+}
+}  // namespace utv

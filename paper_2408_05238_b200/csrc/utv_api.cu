@@ -1523,12 +1523,42 @@ utv_status utv_solve(utv_handle h, int64_t m, int64_t n, int64_t r, const double
   });
 }
 
+// Wide least squares, m < n (reading R21): randUTV of the tall A^T (n x m),
+// A^T V' = U' T', so A = V' T'^T U'^T and eq:simplesoln transposes to
+//   X = U'(:, 0:r) T'11^{-T} V'(:, 0:r)^T B.
+// The lower-triangular solve runs as the existing upper-triangular block solve through the exchange
+// matrix J:  T'11^{-T} c = J (J T'11^T J)^{-1} J c, so X = (U'(:, 0:r) J) (J T'11^T J)^{-1} (J c).
+// U' and V' are explicit (n^2 + m^2 doubles); A and B are left unchanged.
+int64_t lstsq_wide(utv_handle h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                   int64_t ldb, double* X, int64_t ldx, const utv_opts& opts) {
+  cudaStream_t st = h->stream;
+  const size_t nm = (size_t)n * m, mm = (size_t)m * m, nn = (size_t)n * n, mk = (size_t)m * std::max<int64_t>(k, 1);
+  ensure_buf(&h->vbuf, &h->vbuf_doubles, 2 * nm + 2 * mm + nn + 2 * mk);
+  double *At = h->vbuf, *Vp = At + nm, *Up = Vp + mm, *Ur = Up + nn, *Tr = Ur + nm, *Cw = Tr + mm, *Cr = Cw + mk;
+  launch_transpose(st, m, n, A, lda, At, n);
+  Ctx c = make_ctx(h, n, m, k, opts.block);
+  factor_impl(c, n, m, At, n, Vp, m, Up, n, nullptr, 0, 0, opts);
+  if (k > 0) launch_check_finite(st, m, k, B, ldb, h->flag);           // B is not seen by the factorization
+  const int64_t r = finish_factor(c, m, At, n, opts.tau, true);
+  if (k == 0) return r;
+  if (r == 0) { launch_set_zero(st, n, k, X, ldx); return r; }
+  c.gemm(true, false, r, k, m, 1.0, Vp, m, B, ldb, 0.0, Cw, m);       // c = V'(:, 0:r)^T B
+  launch_permute(st, 0, r, k, Cw, m, Cr, m);                          // J c
+  launch_permute(st, 2, r, r, At, n, Tr, m);                          // J T'11^T J (upper)
+  launch_permute(st, 1, n, r, Up, n, Ur, n);                          // U'(:, 0:r) J
+  solve_impl(c, n, r, Tr, m, Ur, n, Cr, m, k, X, ldx);
+  return r;
+}
+
 utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
                      double* X, int64_t ldx, const utv_opts* opts, int64_t* rank) {
   return guarded(h, [&] {
     check_opts(opts);
     if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
-    if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
+    const bool wide = m < n;
+    if (wide && (h->comm || (opts->flags & UTV_HOST_STREAMED)))
+      fail(UTV_ERR_SHAPE, "m < n: single-GPU in-core utv_lstsq only (R21)");
+    if (wide && (opts->flags & UTV_NULLIFY_T12)) fail(UTV_ERR_UNSUPPORTED, "m < n with UTV_NULLIFY_T12");
     check_ld("lda", lda, m);
     if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
     if (h->comm) {                                                     // multi-GPU handle
@@ -1559,6 +1589,13 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     if (hB) { dB = h->stage + off; dldb = m; off += (size_t)m * k; copy2d(st, dB, m, B, ldb, m, k, cudaMemcpyHostToDevice); }
     if (hX) { dX = h->stage + off; dldx = n; off += (size_t)n * k; }
     const int64_t b = opts->block;
+    if (wide) {
+      const int64_t r = lstsq_wide(h, m, n, k, dA, dlda, dB, dldb, dX, dldx, *opts);
+      if (hX) copy2d(st, X, ldx, dX, n, n, k, cudaMemcpyDeviceToHost);
+      if (hX) UTV_CUDA(cudaStreamSynchronize(st));
+      if (rank) *rank = r;
+      return;
+    }
     const bool explicit_v = (opts->flags & UTV_EXPLICIT_V) != 0;
     const bool nullify = (opts->flags & UTV_NULLIFY_T12) != 0;
     FactoredV fv;

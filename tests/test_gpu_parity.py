@@ -274,8 +274,8 @@ def test_host_buffers_end_to_end(utv):
 
 
 def test_error_statuses(utv, h):
-    with pytest.raises(utv.UtvError) as e:
-        utv.lstsq(dev(np.ones((3, 5))), dev(np.ones((3, 1))))
+    with pytest.raises(utv.UtvError) as e:                 # wide: utv_factor keeps m >= n (R4, R21)
+        h.factor(dev(np.ones((3, 5))))
     assert e.value.status == utv.UTV_ERR_SHAPE
     with pytest.raises(utv.UtvError) as e:
         utv.lstsq(dev(np.ones((5, 3))), dev(np.ones((5, 1))), utv.Opts(block=0))

@@ -1,0 +1,113 @@
+"""Wide least squares, m < n (reading R21) on the GPU against the CPU oracle.
+
+Both sides run randUTV on the tall A^T with the same seeded sketch and take
+X = U'(:, 0:r) T'11^{-T} V'(:, 0:r)^T B.  Gates: r identical, x within 1e-9
+of the oracle on exact-rank inputs (where x is also the unique minimum-norm solution), A and B
+left unchanged.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import utv_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def utv():
+    from paper_2408_05238_b200 import build
+    build.build()
+    import paper_2408_05238_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def h(utv):
+    hd = utv.Handle(0)
+    yield hd
+    hd.close()
+
+
+def dev(a):
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    return torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+
+
+def run(utv, h, A, B, b, q, seed, flags=0):
+    Ad, Bd = dev(A), dev(B)
+    A0, B0 = Ad.clone(), Bd.clone()
+    X = utv.colmajor_empty(A.shape[1], Bd.shape[1])
+    r = h.lstsq(Ad, Bd, X, utv.Opts(block=b, power_iters=q, tau=1e-10, seed=seed, flags=flags))
+    torch.cuda.synchronize()
+    assert torch.equal(Ad, A0) and torch.equal(Bd, B0)          # inputs left unchanged (R21)
+    return X.cpu().numpy(), r
+
+
+@pytest.mark.parametrize("m,n,r,b,q,k", [
+    (20, 30, 8, 4, 1, 1),
+    (100, 300, 60, 32, 2, 2),
+    (257, 700, 130, 64, 1, 3),        # ragged last block of A^T's columns
+    (600, 1000, 600, 128, 2, 1),      # full row rank
+    (1000, 2500, 400, 256, 2, 2),
+    (1, 50, 1, 16, 1, 1),
+])
+def test_wide_matches_oracle(utv, h, m, n, r, b, q, k):
+    G = gen.GdMatrix(m, n, r, alpha=1.0, seed=m + 3 * n)
+    B, X0 = G.known_rhs(k=k, consistent=r == m)
+    Xo, ro = oracle.lstsq(G.A, B, b=b, q=q, tau=1e-10, seed=9)
+    X, rg = run(utv, h, G.A, B.reshape(m, -1), b, q, 9)
+    assert rg == ro == r
+    assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
+    assert np.linalg.norm(X - X0) <= 1e-10 * np.linalg.norm(X0)
+
+
+def test_wide_zero_matrix_and_host_buffers(utv, h):
+    X, r = run(utv, h, np.zeros((8, 20)), np.ones((8, 1)), 4, 1, 1)
+    assert r == 0 and not X.any()
+    # host (pageable) A, B, X: staged through device buffers inside the call
+    G = gen.GdMatrix(90, 200, 40, alpha=1.0, seed=4)
+    B, _ = G.known_rhs(k=1)
+    Xo, ro = oracle.lstsq(G.A, B, b=32, q=1, tau=1e-10, seed=2)
+    Ah = torch.from_numpy(np.ascontiguousarray(G.A.T)).t()
+    Bh = torch.from_numpy(np.ascontiguousarray(B.reshape(90, 1).T)).t()
+    Xh = torch.empty((1, 200), dtype=torch.float64).t()
+    rh = h.lstsq(Ah, Bh, Xh, utv.Opts(block=32, power_iters=1, tau=1e-10, seed=2))
+    assert rh == ro == 40
+    assert np.linalg.norm(Xh.numpy() - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
+def test_wide_rejections(utv, h):
+    A = utv.colmajor_empty(16, 40).normal_()
+    B = utv.colmajor_empty(16, 1).normal_()
+    X = utv.colmajor_empty(40, 1)
+    with pytest.raises(utv.UtvError) as e:
+        h.lstsq(A, B, X, utv.Opts(block=8, flags=utv.UTV_NULLIFY_T12))
+    assert e.value.status == utv.UTV_ERR_UNSUPPORTED
+    with pytest.raises(utv.UtvError) as e:                      # utv_factor keeps m >= n (R4)
+        h.factor(A)
+    assert e.value.status == utv.UTV_ERR_SHAPE
+    B[3, 0] = float("nan")
+    with pytest.raises(utv.UtvError) as e:
+        h.lstsq(A, B, X, utv.Opts(block=8))
+    assert e.value.status == utv.UTV_ERR_NUMERICAL
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_wide_random_shapes(utv, h, seed):
+    rng = np.random.default_rng(500 + seed)
+    m = int(rng.integers(2, 400))
+    n = m + int(rng.integers(1, 500))
+    r = int(rng.integers(1, m + 1))
+    b = int(rng.choice([8, 16, 64, 256]))
+    q = int(rng.integers(0, 3))
+    k = int(rng.integers(1, 4))
+    G = gen.GdMatrix(m, n, r, alpha=1.0, seed=seed * 31 + m)
+    B, _ = G.known_rhs(k=k, consistent=r == m)
+    Xo, ro = oracle.lstsq(G.A, B, b=b, q=q, tau=1e-10, seed=seed)
+    X, rg = run(utv, h, G.A, B.reshape(m, -1), b, q, seed)
+    assert rg == ro
+    assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
