@@ -172,6 +172,23 @@ def test_cfg1_parity(utv):
     assert np.linalg.norm(Xg - X0) <= 1e-10 * np.linalg.norm(X0)
 
 
+@pytest.mark.parametrize("matrix", ["gp", "gd3"])
+@pytest.mark.parametrize("scenario", ["ones", "perturbed"])
+def test_cfg1_rhs_scenarios(utv, matrix, scenario):
+    """configs[0] with the paper's right-hand-side scenarios 2 (b = ones) and
+    4 (b = A x with 10% of the entries scaled by 0.999) on Gp and Gd(alpha=3)
+    (SURVEY 8(d) cfg1): x to 1e-9 of the oracle, r identical, and x = the minimum-norm solution."""
+    M = gen.GpMatrix(512, 512, 256) if matrix == "gp" else gen.GdMatrix(512, 512, 256, alpha=3.0)
+    A = M.A
+    B = gen.rhs_ones(512, 1) if scenario == "ones" else gen.rhs_perturbed(A, 1)
+    Xo, ro = oracle.lstsq(A, B, b=64, q=1, tau=1e-10, seed=gen.SKETCH_SEED)
+    Xg, rg = _lstsq_gpu(utv, A, B, 64, 1, seed=gen.SKETCH_SEED)
+    assert rg == ro == 256
+    assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
+    Xp = np.linalg.pinv(A, rcond=1e-10) @ B
+    assert np.linalg.norm(Xg - Xp) <= 1e-9 * np.linalg.norm(Xp)
+
+
 @pytest.mark.parametrize("m,n,r,b,q,kind", [
     (300, 300, 150, 64, 1, "gp"), (333, 257, 100, 64, 2, "gp"), (400, 300, 170, 32, 2, "gd"),
     (256, 256, 256, 64, 0, "full"), (200, 130, 64, 3, 1, "gd"), (600, 520, 261, 256, 1, "gp"),

@@ -298,6 +298,18 @@ def test_lstsq_wide_zero_and_nullify_rejected():
         oracle.lstsq(np.ones((3, 5)), np.ones(3), b=2, q=1, nullify=True)
 
 
+@pytest.mark.parametrize("scenario", ["ones", "perturbed"])
+def test_cfg1_rhs_scenarios_min_norm(scenario):
+    """cfg1 with the paper's RHS scenarios 2 and 4: on the exact-rank
+    Gp matrix the fast-option x is the minimum-norm solution (brute-force pinv)."""
+    G = gen.GpMatrix(512, 512, 256)
+    B = gen.rhs_ones(512, 1) if scenario == "ones" else gen.rhs_perturbed(G.A, 1)
+    X, r = oracle.lstsq(G.A, B, b=64, q=1, tau=1e-10, seed=gen.SKETCH_SEED)
+    assert r == 256
+    Xp = _pinv_solution(G.A, B, 1e-10)
+    assert np.linalg.norm(X - Xp) <= 1e-12 * np.linalg.norm(Xp)
+
+
 def test_rank_edge_cases():
     X, r = oracle.lstsq(np.zeros((10, 6)), np.ones(10), b=4, q=1)
     assert r == 0 and np.all(X == 0.0)
