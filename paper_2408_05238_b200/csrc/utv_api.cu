@@ -1526,18 +1526,23 @@ utv_status utv_solve(utv_handle h, int64_t m, int64_t n, int64_t r, const double
 // Wide least squares, m < n (reading R21): randUTV of the tall A^T (n x m),
 // A^T V' = U' T', so A = V' T'^T U'^T and eq:simplesoln transposes to
 //   X = U'(:, 0:r) T'11^{-T} V'(:, 0:r)^T B.
-// The lower-triangular solve runs as the existing upper-triangular block solve through the exchange
-// matrix J:  T'11^{-T} c = J (J T'11^T J)^{-1} J c, so X = (U'(:, 0:r) J) (J T'11^T J)^{-1} (J c).
-// U' and V' are explicit (n^2 + m^2 doubles); A and B are left unchanged.
+// U' is never formed: T' is upper trapezoidal, so column j < r of A^T V' = U' T' only involves
+// U'(:, 0:r), i.e. A^T V'(:, 0:r) = U'(:, 0:r) T'11 and
+//   X = A^T V'(:, 0:r) T'11^{-1} T'11^{-T} V'(:, 0:r)^T B
+// (A is kept; the minimum-norm seminormal form, error O(kappa(T'11) eps) like the explicit-U'
+// formula -- DESIGN.md R21).  Saves the n x n U' and its 4 n (n m - m^2 / 2) update flops.
+// The lower-triangular solve T'11^{-T} runs as the upper block solve through the exchange matrix J:
+// T'11^{-T} c = J (J T'11^T J)^{-1} J c (solve_impl with "V" = J).
 int64_t lstsq_wide(utv_handle h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                    int64_t ldb, double* X, int64_t ldx, const utv_opts& opts) {
   cudaStream_t st = h->stream;
-  const size_t nm = (size_t)n * m, mm = (size_t)m * m, nn = (size_t)n * n, mk = (size_t)m * std::max<int64_t>(k, 1);
-  ensure_buf(&h->vbuf, &h->vbuf_doubles, 2 * nm + 2 * mm + nn + 2 * mk);
-  double *At = h->vbuf, *Vp = At + nm, *Up = Vp + mm, *Ur = Up + nn, *Tr = Ur + nm, *Cw = Tr + mm, *Cr = Cw + mk;
+  const size_t nm = (size_t)n * m, mm = (size_t)m * m, mk = (size_t)m * std::max<int64_t>(k, 1);
+  ensure_buf(&h->vbuf, &h->vbuf_doubles, nm + 4 * mm + 4 * mk);
+  double *At = h->vbuf, *Vp = At + nm, *Tr = Vp + mm, *Jm = Tr + mm, *Id = Jm + mm, *Cw = Id + mm, *Cr = Cw + mk,
+         *Yw = Cr + mk, *Ww = Yw + mk;
   launch_transpose(st, m, n, A, lda, At, n);
   Ctx c = make_ctx(h, n, m, k, opts.block);
-  factor_impl(c, n, m, At, n, Vp, m, Up, n, nullptr, 0, 0, opts);
+  factor_impl(c, n, m, At, n, Vp, m, nullptr, 0, nullptr, 0, 0, opts);
   if (k > 0) launch_check_finite(st, m, k, B, ldb, h->flag);           // B is not seen by the factorization
   const int64_t r = finish_factor(c, m, At, n, opts.tau, true);
   if (k == 0) return r;
@@ -1545,8 +1550,11 @@ int64_t lstsq_wide(utv_handle h, int64_t m, int64_t n, int64_t k, const double* 
   c.gemm(true, false, r, k, m, 1.0, Vp, m, B, ldb, 0.0, Cw, m);       // c = V'(:, 0:r)^T B
   launch_permute(st, 0, r, k, Cw, m, Cr, m);                          // J c
   launch_permute(st, 2, r, r, At, n, Tr, m);                          // J T'11^T J (upper)
-  launch_permute(st, 1, n, r, Up, n, Ur, n);                          // U'(:, 0:r) J
-  solve_impl(c, n, r, Tr, m, Ur, n, Cr, m, k, X, ldx);
+  launch_set_identity(st, r, r, Id, m);
+  launch_permute(st, 0, r, r, Id, m, Jm, m);                          // J
+  solve_impl(c, r, r, Tr, m, Jm, m, Cr, m, k, Yw, m);                 // y = T'11^{-T} c
+  solve_impl(c, m, r, At, n, Vp, m, Yw, m, k, Ww, m);                 // w = V'(:, 0:r) T'11^{-1} y
+  c.gemm(true, false, n, k, m, 1.0, A, lda, Ww, m, 0.0, X, ldx);      // X = A^T w
   return r;
 }
 
