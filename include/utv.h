@@ -150,7 +150,8 @@ utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const d
  * (left unchanged), a host X is written and the call returns after X has landed.
  * Wide A (m < n, reading R21): randUTV of the tall A^T (A^T V' = U' T') and
  * X = U'(:, 0:r) T'11^{-T} V'(:, 0:r)^T B, evaluated without forming U' as
- * A^T V'(:, 0:r) T'11^{-1} T'11^{-T} V'(:, 0:r)^T B (workspace about n m + 4 m^2 doubles);
+ * A^T V'(:, 0:r) T'11^{-1} T'11^{-T} V'(:, 0:r)^T B with V' factored (workspace about
+ * n m + 3.5 m^2 doubles);
  * A and B are left unchanged; single-GPU in-core only (multi-GPU / UTV_HOST_STREAMED ->
  * UTV_ERR_SHAPE, UTV_NULLIFY_T12 -> UTV_ERR_UNSUPPORTED).
  */

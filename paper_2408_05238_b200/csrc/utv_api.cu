@@ -1530,31 +1530,50 @@ utv_status utv_solve(utv_handle h, int64_t m, int64_t n, int64_t r, const double
 // U'(:, 0:r), i.e. A^T V'(:, 0:r) = U'(:, 0:r) T'11 and
 //   X = A^T V'(:, 0:r) T'11^{-1} T'11^{-T} V'(:, 0:r)^T B
 // (A is kept; the minimum-norm seminormal form, error O(kappa(T'11) eps) like the explicit-U'
-// formula -- DESIGN.md R21).  Saves the n x n U' and its 4 n (n m - m^2 / 2) update flops.
+// formula -- DESIGN.md R21).  Saves the n x n U' and its 4 n (n m - m^2 / 2) update flops; V' stays
+// factored (its reflectors are applied transposed to B, forward to the solution).
 // The lower-triangular solve T'11^{-T} runs as the upper block solve through the exchange matrix J:
 // T'11^{-T} c = J (J T'11^T J)^{-1} J c (solve_impl with "V" = J).
 int64_t lstsq_wide(utv_handle h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                    int64_t ldb, double* X, int64_t ldx, const utv_opts& opts) {
   cudaStream_t st = h->stream;
   const size_t nm = (size_t)n * m, mm = (size_t)m * m, mk = (size_t)m * std::max<int64_t>(k, 1);
-  ensure_buf(&h->vbuf, &h->vbuf_doubles, nm + 4 * mm + 4 * mk);
-  double *At = h->vbuf, *Vp = At + nm, *Tr = Vp + mm, *Jm = Tr + mm, *Id = Jm + mm, *Cw = Id + mm, *Cr = Cw + mk,
-         *Yw = Cr + mk, *Ww = Yw + mk;
+  // V' is kept factored: V' = Q_1 ... Q_s blockdiag(V_s)
+  const int64_t b = opts.block, nsteps = (m + b - 1) / b;
+  const size_t wdbl = factored_w_doubles(m, b), tdbl = (size_t)nsteps * b * b;
+  ensure_buf(&h->vbuf, &h->vbuf_doubles, nm + wdbl + 2 * tdbl + 3 * mm + 4 * mk + 64);
+  double *At = h->vbuf, *Tr = At + nm, *Jm = Tr + mm, *Id = Jm + mm, *Cw = Id + mm, *Cr = Cw + mk, *Yw = Cr + mk,
+         *Ww = Yw + mk;
+  FactoredV fv;
+  fv.W = Ww; fv.T = fv.W + wdbl; fv.Vs = fv.T + tdbl;
   launch_transpose(st, m, n, A, lda, At, n);
-  Ctx c = make_ctx(h, n, m, k, opts.block);
-  factor_impl(c, n, m, At, n, Vp, m, nullptr, 0, nullptr, 0, 0, opts);
+  Ctx c = make_ctx(h, n, m, k, b);
+  factor_impl(c, n, m, At, n, nullptr, 0, nullptr, 0, nullptr, 0, 0, opts, &fv);
   if (k > 0) launch_check_finite(st, m, k, B, ldb, h->flag);           // B is not seen by the factorization
   const int64_t r = finish_factor(c, m, At, n, opts.tau, true);
   if (k == 0) return r;
   if (r == 0) { launch_set_zero(st, n, k, X, ldx); return r; }
-  c.gemm(true, false, r, k, m, 1.0, Vp, m, B, ldb, 0.0, Cw, m);       // c = V'(:, 0:r)^T B
-  launch_permute(st, 0, r, k, Cw, m, Cr, m);                          // J c
+  // c = V'(:, 0:r)^T B = (blockdiag(V_s)^T Q_s^T ... Q_1^T B)(0:r)
+  double *tmp = c.at(c.L.Z1), *tmp2 = c.at(c.L.Z2);
+  launch_copy(st, m, k, B, ldb, Cw, m);
+  for (size_t i = 0; i < fv.woff.size(); ++i) {                        // Q_i^T = I - W_i T_i^T W_i^T
+    const int64_t j0 = fv.j0[i], np = fv.np[i];
+    const double* W = fv.W + fv.woff[i];
+    c.gemm(true, false, b, k, np, 1.0, W, np, Cw + j0, m, 0.0, tmp, b);
+    c.gemm(true, false, b, k, b, 1.0, fv.T + (size_t)(j0 / b) * b * b, b, tmp, b, 0.0, tmp2, b);
+    c.gemm(false, false, np, k, b, -1.0, W, np, tmp2, b, 1.0, Cw + j0, m);
+  }
+  for (int64_t j0 = 0, step = 0; j0 < r; j0 += b, ++step) {             // V_s^T on the blocks 0:r
+    const int64_t bw = std::min(b, m - j0);
+    c.gemm(true, false, bw, k, bw, 1.0, fv.Vs + (size_t)step * b * b, b, Cw + j0, m, 0.0, Yw + j0, m);
+  }
+  launch_permute(st, 0, r, k, Yw, m, Cr, m);                          // J c
   launch_permute(st, 2, r, r, At, n, Tr, m);                          // J T'11^T J (upper)
   launch_set_identity(st, r, r, Id, m);
   launch_permute(st, 0, r, r, Id, m, Jm, m);                          // J
   solve_impl(c, r, r, Tr, m, Jm, m, Cr, m, k, Yw, m);                 // y = T'11^{-T} c
-  solve_impl(c, m, r, At, n, Vp, m, Yw, m, k, Ww, m);                 // w = V'(:, 0:r) T'11^{-1} y
-  c.gemm(true, false, n, k, m, 1.0, A, lda, Ww, m, 0.0, X, ldx);      // X = A^T w
+  solve_factored(c, m, r, At, n, Yw, m, k, Cw, m, fv, b);             // w = V'(:, 0:r) T'11^{-1} y
+  c.gemm(true, false, n, k, m, 1.0, A, lda, Cw, m, 0.0, X, ldx);      // X = A^T w
   return r;
 }
 
