@@ -51,3 +51,18 @@ def test_big_gemm_selection(bench, tmp_path):
     st = bench.big_gemm_stats(str(p))
     assert st["launches"] == 1
     assert abs(st["tflops"] - 3.5e11 / 10e-3 / 1e12) < 1e-9
+
+
+def test_hbm_kernels_gbs(bench):
+    """hbm_kernels: algorithmic bytes / summed launch time against the measured HBM copy peak;
+    families without recorded bytes or time are left out."""
+    prof = {"sketch": {"ms": 10.0, "bytes": 6.4e10, "launches": 5},
+            "panel": {"ms": 2.0, "bytes": 0.0, "launches": 3},
+            "solve": {"ms": 0.0, "bytes": 1e6, "launches": 1},
+            "gemm": {"ms": 1.0, "bytes": 1e12, "launches": 1}}
+    out = bench.hbm_kernels(prof)
+    assert set(out) >= {"peak_gbs", "peak_source", "sketch"}
+    assert "panel" not in out and "solve" not in out and "gemm" not in out
+    assert out["sketch"]["gbs"] == pytest.approx(6400.0)
+    assert out["sketch"]["frac"] == pytest.approx(6400.0 / out["peak_gbs"])
+    assert out["peak_gbs"] > 1000.0
