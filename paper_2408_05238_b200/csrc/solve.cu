@@ -42,30 +42,45 @@ __global__ void rank_kernel(int64_t n, const double* __restrict__ T, int64_t ldt
 }
 
 // Column-oriented back substitution on one diagonal block (<= 256 rows), k RHS in chunks of 16.
-constexpr int TS_ROWS = 256, TS_K = 16;
-__global__ void trsv_block_kernel(int64_t j0, int64_t j1, const double* __restrict__ T, int64_t ldt,
-                                  double* __restrict__ Z, int64_t ldz, int64_t k) {
+// Thread p owns row p.  The block's columns are read in batches of TS_B from the bottom, each thread
+// holding its TS_B entries T(p, i) in registers, so the dependent global-load latency is paid once
+// per batch instead of once per column (the arithmetic and its order are unchanged).
+constexpr int TS_ROWS = 256, TS_K = 16, TS_B = 32;
+__global__ void __launch_bounds__(TS_ROWS) trsv_block_kernel(int64_t j0, int64_t j1, const double* __restrict__ T,
+                                                             int64_t ldt, double* __restrict__ Z, int64_t ldz,
+                                                             int64_t k) {
   __shared__ double z[TS_K][TS_ROWS];
   const int bs = (int)(j1 - j0);
+  const int p = threadIdx.x;
   for (int64_t c0 = 0; c0 < k; c0 += TS_K) {
     const int kc = (int)((k - c0) < TS_K ? (k - c0) : TS_K);
     for (int e = threadIdx.x; e < bs * kc; e += blockDim.x) {
-      const int p = e % bs, c = e / bs;
-      z[c][p] = Z[cm(j0 + p, c0 + c, ldz)];
+      const int q = e % bs, c = e / bs;
+      z[c][q] = Z[cm(j0 + q, c0 + c, ldz)];
     }
     __syncthreads();
-    for (int i = bs - 1; i >= 0; --i) {
-      if (threadIdx.x < kc) z[threadIdx.x][i] /= T[cm(j0 + i, j0 + i, ldt)];
-      __syncthreads();
-      for (int e = threadIdx.x; e < i * kc; e += blockDim.x) {
-        const int p = e % i, c = e / i;
-        z[c][p] -= T[cm(j0 + p, j0 + i, ldt)] * z[c][i];
+    for (int cb = ((bs - 1) / TS_B) * TS_B; cb >= 0; cb -= TS_B) {
+      double t[TS_B];
+#pragma unroll
+      for (int u = 0; u < TS_B; ++u) {
+        const int i = cb + u;
+        t[u] = (i < bs && p <= i) ? T[cm(j0 + p, j0 + i, ldt)] : 0.0;
       }
-      __syncthreads();
+#pragma unroll
+      for (int u = TS_B - 1; u >= 0; --u) {
+        const int i = cb + u;
+        if (i >= bs) continue;                                   // uniform over the block
+        if (p == i)
+          for (int c = 0; c < kc; ++c) z[c][i] /= t[u];
+        __syncthreads();
+        if (p < i)
+          for (int c = 0; c < kc; ++c) z[c][p] -= t[u] * z[c][i];
+        __syncthreads();
+      }
     }
     for (int e = threadIdx.x; e < bs * kc; e += blockDim.x) {
-      const int p = e % bs, c = e / bs;
-      Z[cm(j0 + p, c0 + c, ldz)] = z[c][p];
+      const int q = e % bs, c = e / bs;
+      Z[cm(j0 + q, c0 + c, ldz)] = z[c][q];
     }
     __syncthreads();
   }
@@ -81,8 +96,9 @@ void launch_rank(cudaStream_t st, int64_t n, const double* T, int64_t ldt, doubl
 void launch_trsv_block(cudaStream_t st, int64_t j0, int64_t j1, const double* T, int64_t ldt, double* Z, int64_t ldz,
                        int64_t k) {
   if (j1 <= j0 || k <= 0) return;
-  ProfScope prof(st, kProfSolve, 1, (double)(j1 - j0) * (j1 - j0) * k, 8.0 * (j1 - j0) * (j1 - j0) / 2);
-  trsv_block_kernel<<<1, 256, 0, st>>>(j0, j1, T, ldt, Z, ldz, k);
+  ProfScope prof(st, kProfSolve, 1, (double)(j1 - j0) * (j1 - j0) * k,
+                 8.0 * (j1 - j0) * (j1 - j0) / 2 + 16.0 * (j1 - j0) * k);
+  trsv_block_kernel<<<1, TS_ROWS, 0, st>>>(j0, j1, T, ldt, Z, ldz, k);
   UTV_CUDA(cudaGetLastError());
 }
 
