@@ -41,17 +41,18 @@ __global__ void rank_kernel(int64_t n, const double* __restrict__ T, int64_t ldt
   }
 }
 
-// Column-oriented back substitution on one diagonal block (<= 256 rows), k RHS in chunks of 16.
-// Thread p owns row p.  The block's columns are read in batches of TS_B from the bottom, each thread
-// holding its TS_B entries T(p, i) in registers, so the dependent global-load latency is paid once
-// per batch instead of once per column (the arithmetic and its order are unchanged).
-constexpr int TS_ROWS = 256, TS_K = 16, TS_B = 32;
+// Back substitution on one diagonal block (<= 256 rows), k RHS in chunks of 16, in sub-blocks of 32
+// from the bottom: warp 0 solves the 32 x 32 diagonal triangle with lane l owning row l (the pivot
+// broadcast by shuffles, no block barrier per column), then every thread p above the sub-block
+// subtracts its 32 terms T(p, i) z(i).  Per element the operations and their order (i descending,
+// divide when all later columns are in) are those of plain column back substitution.
+constexpr int TS_ROWS = 256, TS_K = 16, TS_SB = 32;
 __global__ void __launch_bounds__(TS_ROWS) trsv_block_kernel(int64_t j0, int64_t j1, const double* __restrict__ T,
                                                              int64_t ldt, double* __restrict__ Z, int64_t ldz,
                                                              int64_t k) {
   __shared__ double z[TS_K][TS_ROWS];
   const int bs = (int)(j1 - j0);
-  const int p = threadIdx.x;
+  const int p = threadIdx.x, lane = p & 31;
   for (int64_t c0 = 0; c0 < k; c0 += TS_K) {
     const int kc = (int)((k - c0) < TS_K ? (k - c0) : TS_K);
     for (int e = threadIdx.x; e < bs * kc; e += blockDim.x) {
@@ -59,24 +60,39 @@ __global__ void __launch_bounds__(TS_ROWS) trsv_block_kernel(int64_t j0, int64_t
       z[c][q] = Z[cm(j0 + q, c0 + c, ldz)];
     }
     __syncthreads();
-    for (int cb = ((bs - 1) / TS_B) * TS_B; cb >= 0; cb -= TS_B) {
-      double t[TS_B];
+    for (int sb = ((bs - 1) / TS_SB) * TS_SB; sb >= 0; sb -= TS_SB) {
+      const int w = (bs - sb) < TS_SB ? (bs - sb) : TS_SB;
+      if (p < 32) {                                                    // diagonal 32 x 32 triangle
+        double t[TS_SB];
 #pragma unroll
-      for (int u = 0; u < TS_B; ++u) {
-        const int i = cb + u;
-        t[u] = (i < bs && p <= i) ? T[cm(j0 + p, j0 + i, ldt)] : 0.0;
-      }
+        for (int u = 0; u < TS_SB; ++u)
+          t[u] = (u < w && lane < w && lane <= u) ? T[cm(j0 + sb + lane, j0 + sb + u, ldt)] : 1.0;
+        for (int c = 0; c < kc; ++c) {
+          double zl = lane < w ? z[c][sb + lane] : 0.0;
 #pragma unroll
-      for (int u = TS_B - 1; u >= 0; --u) {
-        const int i = cb + u;
-        if (i >= bs) continue;                                   // uniform over the block
-        if (p == i)
-          for (int c = 0; c < kc; ++c) z[c][i] /= t[u];
-        __syncthreads();
-        if (p < i)
-          for (int c = 0; c < kc; ++c) z[c][p] -= t[u] * z[c][i];
-        __syncthreads();
+          for (int u = TS_SB - 1; u >= 0; --u) {
+            if (u >= w) continue;                                      // uniform
+            if (lane == u) zl /= t[u];
+            const double zi = __shfl_sync(0xffffffffu, zl, u);
+            if (lane < u) zl -= t[u] * zi;
+          }
+          if (lane < w) z[c][sb + lane] = zl;
+        }
       }
+      __syncthreads();
+      if (p < sb) {                                                    // rows above: 32 terms each
+        double t[TS_SB];
+#pragma unroll
+        for (int u = 0; u < TS_SB; ++u) t[u] = u < w ? T[cm(j0 + p, j0 + sb + u, ldt)] : 0.0;
+        for (int c = 0; c < kc; ++c) {
+          double acc = z[c][p];
+#pragma unroll
+          for (int u = TS_SB - 1; u >= 0; --u)
+            if (u < w) acc -= t[u] * z[c][sb + u];
+          z[c][p] = acc;
+        }
+      }
+      __syncthreads();
     }
     for (int e = threadIdx.x; e < bs * kc; e += blockDim.x) {
       const int q = e % bs, c = e / bs;
