@@ -342,3 +342,20 @@ def test_lstsq_random_shapes(utv, m, n, r, b, q, k):
     Xg, rg = _lstsq_gpu(utv, M.A, B, b, q, seed=13)
     assert rg == ro
     assert np.linalg.norm(Xg - Xo) <= 1e-9 * max(np.linalg.norm(Xo), 1e-300)
+
+
+@pytest.mark.parametrize("n,k", [(1, 1), (31, 5), (33, 16), (256, 17), (257, 40), (700, 3)])
+def test_trsm_upper_blocks(utv, h, n, k):
+    """a9's block back substitution (utv_trsm_upper): 32-row sub-blocks, ragged tails and RHS
+    chunks of 16, against scipy's triangular solve (a library routine, not the oracle)."""
+    from scipy.linalg import solve_triangular
+    rng = np.random.default_rng(n * 100 + k)
+    T = np.triu(rng.standard_normal((n + 3, n + 3))) / np.sqrt(n + 3) + 2.0 * np.eye(n + 3)   # ld > n
+    Z = rng.standard_normal((n, k))
+    ref = solve_triangular(T[:n, :n], Z, lower=False)
+    Td = dev(T)
+    Zd = dev(Z)
+    h.trsm_upper(Td, Zd)
+    torch.cuda.synchronize()
+    got = Zd.cpu().numpy()
+    assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
