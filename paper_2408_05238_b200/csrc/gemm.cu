@@ -400,7 +400,7 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
   const int64_t tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
-  constexpr int64_t GROUP_M = 16;
+  const int64_t GROUP_M = (mn_3d >> 8) ? (mn_3d >> 8) : 16;    // raster group height (tile rows)
   const int64_t pid = blockIdx.x;
   const int64_t per_group = GROUP_M * tiles_n;
   const int64_t first_m = (pid / per_group) * GROUP_M;
@@ -633,7 +633,8 @@ bool launch_tma_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   if (!make_tmap(&ta_map, A, TA ? K : M, TA ? M : K, lda, !TA, CF::BM, &a3)) return false;
   // B operand (K x N): !TB -> stored K x N (K-major); TB -> stored N x K (MN-major)
   if (!make_tmap(&tb_map, B, TB ? N : K, TB ? K : N, ldb, TB, CF::BN, &b3)) return false;
-  const int mn_3d = (a3 ? 1 : 0) | (b3 ? 2 : 0);
+  static const int group_m = [] { const char* e = std::getenv("UTV_GEMM_GROUP_M"); return e ? std::atoi(e) : 0; }();
+  const int mn_3d = (a3 ? 1 : 0) | (b3 ? 2 : 0) | (group_m << 8);
   static std::atomic<unsigned long long> attr_set{0};
   auto kern = dgemm_tma_kernel<TA, TB, ID>;
   ensure_smem_attr(kern, (int)CF::SMEM, attr_set);
