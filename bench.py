@@ -191,46 +191,68 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_baseline(sample_n: int = 2048, threads: int | None = None):
-    """The oracle as it stands, on a bounded sample of the cfg3 recipe (rank n/2, b=256, q=2)."""
+def sample_shape(config: str, sample_n: int):
+    """A bounded CPU sample of a config's recipe: n = sample_n columns, the config's m/n and r/n
+    ratios, its q and k, b = min(b, n)."""
+    m, n, r, b, q, k = CONFIGS[config]
+    ns = min(sample_n, n)
+    return max(ns, round(m / n * ns)), ns, max(1, round(r / n * ns)), min(b, ns), q, k
+
+
+def cpu_baseline(sample_n: int = 2048, threads: int | None = None, config: str = "cfg3"):
+    """The oracle as it stands, on a bounded sample of the config's recipe (sample_shape)."""
     import numpy as np
     import oracle
     import utv_inputs as gen
     if threads:
         oracle.set_threads(threads)
-    G = gen.GpMatrix(sample_n, sample_n, sample_n // 2)
-    B, X0 = G.known_rhs(k=1)
+    m, n, r, b, q, k = sample_shape(config, sample_n)
+    G = gen.GpMatrix(m, n, r)
+    B, X0 = G.known_rhs(k=k, consistent=m < 2 * r)
     t0 = time.perf_counter()
-    X, r = oracle.lstsq(G.A, B, b=256, q=2, tau=1e-10, seed=gen.SKETCH_SEED)
+    X, rk = oracle.lstsq(G.A, B, b=b, q=q, tau=1e-10, seed=gen.SKETCH_SEED)
     dt = time.perf_counter() - t0
-    F = f_alg(sample_n, sample_n, 256, 2, 1, r)
-    err = float(np.linalg.norm(X - X0) / np.linalg.norm(X0))
+    F = f_alg(m, n, b, q, k, rk)
+    err = float(np.linalg.norm(X - X0.reshape(X.shape)) / np.linalg.norm(X0))
     return {"value": F / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": f"oracle lstsq on the cfg3 recipe at n={sample_n} (rank {sample_n // 2}, b=256, q=2, k=1): "
+            "sample": f"oracle lstsq on the {config} recipe at m={m}, n={n} (rank {r}, b={b}, q={q}, k={k}): "
                       f"{dt:.2f} s, F_alg={F:.3e}, rel err vs x0 {err:.1e}",
-            "seconds": dt}
+            "seconds": dt, "flops": F}
+
+
+def config_dict(config: str, world: int, use_dist: bool):
+    """The bench line's `config` (identical on both arms)."""
+    m, n, r_true, b, q, k = CONFIGS[config]
+    return {"workload": (f"{config}: square n={n}" if m == n else f"{config}: tall m={m} x n={n}")
+                        + f" rank {r_true}, b={b}, q={q}, k={k} (paper generator "
+                        "P:2436-2448, known min-norm solution)", "m": m, "n": n, "rank": r_true, "block": b,
+            "power_iters": q, "rhs": k,
+            "parallelism": f"blockcyclic{world}" if use_dist else "single",
+            "l2": "inputs (8mn = %.1f GB) >> 126 MB L2; no flush needed" % (8 * m * n / 1e9),
+            "step": ("restore the rank's A shard from a pristine device copy (D2D) + utv_lstsq on a "
+                     "utv_create_dist handle (block-cyclic columns, NCCL)") if use_dist else
+                    "restore A,B from a pristine device copy (D2D) + utv_lstsq"}
 
 
 def run_reference(args):
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return
-    import oracle
     n_s = args.ref_n
-    times = []
+    times, cb = [], None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(n_s)
+        cb = cpu_baseline(n_s, config=args.config)
         if i >= args.warmup:
             times.append(cb["seconds"])
     t = sum(times) / len(times)
-    F = f_alg(n_s, n_s, 256, 2, 1, n_s // 2)
-    val = F / t / 1e12
+    val = cb["flops"] / t / 1e12
     out = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"{args.config} recipe, bounded CPU sample n={n_s}", "sample_n": n_s},
-           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": oracle.get_threads(), "kind": "oracle",
-                            "sample": f"oracle lstsq, cfg3 recipe at n={n_s} (rank {n_s // 2}, b=256, q=2)"},
+           "config": config_dict(args.config, args.gpus, args.gpus > 1 or args.force_dist),
+           "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cb["cores"], "kind": "oracle",
+                            "sample": "each step: " + cb["sample"].split(":")[0] + " -- a bounded sample of "
+                                      "the workload, F_alg of the sample / its time"},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -404,15 +426,7 @@ def run_ours(args):
         "scaled_time": t * 1e12 / float(n) ** 3,          # the paper's scaled time: t 1e12 / n^3
         "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": (f"{args.config}: square n={n}" if m == n else f"{args.config}: tall m={m} x n={n}")
-                               + f" rank {r_true}, b={b}, q={q}, k={k} (paper generator "
-                               "P:2436-2448, known min-norm solution)", "m": m, "n": n, "rank": r_true, "block": b,
-                   "power_iters": q, "rhs": k,
-                   "parallelism": f"blockcyclic{world}" if use_dist else "single",
-                   "l2": "inputs (8mn = %.1f GB) >> 126 MB L2; no flush needed" % (8 * m * n / 1e9),
-                   "step": ("restore the rank's A shard from a pristine device copy (D2D) + utv_lstsq on a "
-                            "utv_create_dist handle (block-cyclic columns, NCCL)") if use_dist else
-                           "restore A,B from a pristine device copy (D2D) + utv_lstsq"},
+        "config": config_dict(args.config, world, use_dist),
         "value_definition": "F_alg (SURVEY App. B, fixed workload incl. explicit-V accumulation) / "
                             "time-to-solution; executed_tflops counts the flops actually executed",
         "executed_tflops": executed_tflops, "executed_flops": F_exec,
@@ -443,7 +457,8 @@ def run_ours(args):
     if e2e:
         out["e2e"] = e2e
     if not args.no_cpu_baseline and world >= 1 and rank == 0 and world == 1:
-        out["cpu_baseline"] = {k2: v for k2, v in cpu_baseline(args.cpu_n).items() if k2 != "seconds"}
+        cb = cpu_baseline(args.cpu_n, config=args.config)
+        out["cpu_baseline"] = {k2: v for k2, v in cb.items() if k2 not in ("seconds", "flops")}
     print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
