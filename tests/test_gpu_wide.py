@@ -106,6 +106,17 @@ def test_wide_rejections(utv, h):
     with pytest.raises(utv.UtvError) as e:                      # utv_factor keeps m >= n (R4)
         h.factor(A)
     assert e.value.status == utv.UTV_ERR_SHAPE
+    Ah = torch.empty((40, 16), dtype=torch.float64).t().normal_()   # out of core: m >= n only
+    with pytest.raises(utv.UtvError) as e:
+        h.lstsq(Ah, B, X, utv.Opts(block=8, flags=utv.UTV_HOST_STREAMED))
+    assert e.value.status == utv.UTV_ERR_SHAPE
+    hs = utv.local_group(1)                                         # multi-GPU: m >= n only
+    try:
+        with pytest.raises(utv.UtvError) as e:
+            hs[0].lstsq(A, B, X, utv.Opts(block=8))
+        assert e.value.status == utv.UTV_ERR_SHAPE
+    finally:
+        hs[0].close()
     B[3, 0] = float("nan")
     with pytest.raises(utv.UtvError) as e:
         h.lstsq(A, B, X, utv.Opts(block=8))
