@@ -138,3 +138,20 @@ def test_wide_random_shapes(utv, h, seed):
     X, rg = run(utv, h, G.A, B.reshape(m, -1), b, q, seed)
     assert rg == ro
     assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
+def test_wide_large_known_solution(utv, h):
+    """10000 x 20000 rank 5000 (Gp generated on the device; m = 2r, so b carries a residual r_perp
+    orthogonal to range(A)): properties that hold at any size -- r exact, x = the known minimum-norm
+    solution x0, and the normal-equation residual of the north star."""
+    m, n, r = 10000, 20000, 5000
+    At, Bm, X0 = gen.gp_torch(m, n, r, device="cuda", k=2)
+    A = At.t()
+    B = utv.colmajor(Bm)
+    X = utv.colmajor_empty(n, 2)
+    rk = h.lstsq(A, B, X, utv.Opts(block=256, power_iters=2, tau=1e-10, seed=1))
+    torch.cuda.synchronize()
+    assert rk == r
+    assert (torch.linalg.norm(X - X0) / torch.linalg.norm(X0)).item() <= 1e-10
+    ne = torch.linalg.norm(A.t() @ (A @ X - Bm)) / (torch.linalg.norm(A) ** 2 * torch.linalg.norm(X))
+    assert ne.item() <= 1e-12
