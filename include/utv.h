@@ -36,7 +36,7 @@ typedef enum {
                                 guard for wide matrices is garbled: R4), multi-GPU or out-of-core lstsq */
   UTV_ERR_ALLOC = -3,        /* device / pinned allocation failed */
   UTV_ERR_CUDA = -4,         /* a CUDA runtime call failed */
-  UTV_ERR_NCCL = -5,         /* reserved: multi-GPU communication failure */
+  UTV_ERR_NCCL = -5,         /* multi-GPU communication failure (peer aborted, NCCL error, timeout) */
   UTV_ERR_NUMERICAL = -6,    /* NaN/Inf in A or B, or the b x b Jacobi SVD exceeded 30 sweeps */
   UTV_ERR_UNSUPPORTED = -7   /* a feature of this ABI that this build does not provide */
 } utv_status;
@@ -46,7 +46,8 @@ enum {
   UTV_WANT_U = 2u,           /* build U explicitly (v21t semantics) when U != NULL */
   UTV_NULLIFY_T12 = 4u,      /* Nullify_top_right_part_of_T after Compute_rank (fig:alg_nullify_t12) */
   UTV_HOST_STREAMED = 8u,    /* utv_lstsq: A stays in host memory, streamed through HBM (out of core) */
-  UTV_EXPLICIT_V = 16u       /* utv_lstsq: accumulate V explicitly (default: factored V, see below) */
+  UTV_EXPLICIT_V = 16u,      /* utv_lstsq: accumulate V explicitly (default: factored V, see below) */
+  UTV_KEEP_FACTORS = 32u     /* keep U and V in factored form on the handle for utv_solve_rhs */
 };
 
 /* Parameters of randUTV(A, q, n_b) (fig:alg_utv) and Compute_rank. */
@@ -71,8 +72,14 @@ utv_status utv_create(utv_handle* handle, int device, void* stream);
  * U^T B; X (n x k, device) is written, identical on every rank; *rank is identical on every rank.
  * All ranks must make the same calls with the same m, n, k, opts (collectives in lock step).
  * Fast option with factored V only (UTV_NULLIFY_T12 / UTV_EXPLICIT_V / UTV_HOST_STREAMED ->
- * UTV_ERR_UNSUPPORTED); utv_factor on such a handle -> UTV_ERR_UNSUPPORTED.  A communication
- * failure returns UTV_ERR_NCCL.
+ * UTV_ERR_UNSUPPORTED); utv_factor on such a handle -> UTV_ERR_UNSUPPORTED.
+ * Failures: the ranks first agree on the call (one AllReduce of a flag after every rank has checked
+ * its arguments and reserved its device memory), so a rank-local argument / allocation error fails
+ * the call on EVERY rank (the peers get UTV_ERR_ARG) and the handle stays usable; NaN / Inf and
+ * Jacobi failures are AllReduce-d as well (every rank returns UTV_ERR_NUMERICAL).  A later failure
+ * (CUDA error, an NCCL asynchronous error, or no progress for UTV_COMM_TIMEOUT_S seconds, default
+ * 3600) aborts the communicator (ncclCommAbort, which ends the rank's in-flight collectives) and
+ * returns UTV_ERR_NCCL / UTV_ERR_CUDA; such a handle must be destroyed.
  */
 /* NCCL unique id (128 bytes) for utv_create_dist; call on one rank and share it (e.g. through
  * torch.distributed).  libnccl.so.2 is loaded at run time; UTV_ERR_NCCL if it is unavailable. */
@@ -135,6 +142,29 @@ utv_status utv_factor(utv_handle handle, int64_t m, int64_t n, double* A, int64_
 utv_status utv_solve(utv_handle handle, int64_t m, int64_t n, int64_t r, const double* T,
                      int64_t ldt, const double* V, int64_t ldv, const double* C, int64_t ldc,
                      int64_t k, double* X, int64_t ldx);
+
+/*
+ * Reuse of a factorization for a new right-hand side (the reuse that the paper's
+ * v23t "cannot" offer, without the m x m explicit U of v21t).
+ * A utv_factor or utv_lstsq call with opts->flags & UTV_KEEP_FACTORS leaves on the handle every
+ * step's block reflectors (W_U, T_U), (W_V, T_V) and the small SVD factors U_s, V_s -- about
+ * m n doubles (sum of the m' x b panels) + n^2 / 2 -- so that
+ *   U = Q_U,1 ... Q_U,s blockdiag(U_s,i),   V = Q_V,1 ... Q_V,s blockdiag(V_s,i)
+ * can be applied later.  Supported: single-GPU in-core calls with DEVICE A (T stays in the
+ * caller's A), and multi-GPU handles (T stays in each rank's shard); UTV_NULLIFY_T12,
+ * UTV_HOST_STREAMED, host A and wide A (m < n) with UTV_KEEP_FACTORS -> UTV_ERR_UNSUPPORTED.
+ * The factors stay valid until the next UTV_KEEP_FACTORS call or utv_destroy.
+ *
+ * utv_solve_rhs: X (n x k, ldx >= n) = V(:, 0:r) T(0:r, 0:r)^{-1} (U^T B)(0:r, :) for a NEW B
+ * (m x k, ldb >= m; overwritten by U^T B), with r, m, n those of the kept factorization (m, n
+ * must match: UTV_ERR_SHAPE).  T (ldt) is the T that factorization left in A (the rank's shard
+ * on a multi-GPU handle; B and X are then replicated on every rank).  *rank (if non-NULL) = r.
+ * UTV_ERR_ARG if no factorization was kept.  No host synchronisation (multi-GPU: one per block of
+ * the distributed triangular solve).
+ */
+utv_status utv_solve_rhs(utv_handle handle, int64_t m, int64_t n, int64_t k, const double* T,
+                         int64_t ldt, double* B, int64_t ldb, double* X, int64_t ldx,
+                         int64_t* rank);
 
 /*
  * Solve_linear_system, fast option (fig:alg_axb P:1075-1108 without the Nullify line;

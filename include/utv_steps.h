@@ -67,6 +67,26 @@ utv_status utv_rank(utv_handle handle, int64_t n, const double* T, int64_t ldt, 
  * (multi-GPU path, where diag(T) is spread over the column owners); synchronises. */
 utv_status utv_rank_diag(utv_handle handle, int64_t n, const double* d, double tau, int64_t* rank);
 
+/* ---- test / tuning knobs ---------------------------------------------------------------
+ * Process-wide switches that force one implementation choice, so that parity tests can reach
+ * on small inputs the code paths that only full-size problems take (and benchmarks can sweep
+ * them).  They change how a result is computed, never what is computed.  value < 0 (or 0 where
+ * stated) restores the automatic choice.  Not synchronised: set them while no call is running.
+ *   UTV_TUNE_GEMM_CFG     DMMA GEMM tile configuration 0..5 (csrc/gemm.cu Shape<> table)
+ *   UTV_TUNE_GEMM_SPLITS  split-K factor >= 1 (0 = cost model), clamped to the workspace
+ *   UTV_TUNE_GEMM_PATH    1 = the cp.async kernel instead of the TMA kernel (0 = automatic)
+ *   UTV_TUNE_QR_GLOBAL    1 = the global-memory sub-panel kernel of a3/a5 at any panel height
+ *   UTV_TUNE_QR_CTAS      cap on the cooperative CTAs of a sub-panel launch (0 = automatic)
+ * Returns UTV_ERR_ARG for an unknown key; *old (if non-NULL) gets the previous value. */
+enum {
+  UTV_TUNE_GEMM_CFG = 1,
+  UTV_TUNE_GEMM_SPLITS = 2,
+  UTV_TUNE_GEMM_PATH = 3,
+  UTV_TUNE_QR_GLOBAL = 4,
+  UTV_TUNE_QR_CTAS = 5
+};
+utv_status utv_tune(int key, int64_t value, int64_t* old);
+
 /* ---- instrumentation (bench.py) -----------------------------------------------------
  * When enabled, every kernel launch of the library on this handle is bracketed by CUDA events
  * on the handle's stream and tagged with a family; flops / bytes are the ALGORITHMIC counts of

@@ -21,14 +21,14 @@ LIB_PATH = os.path.join(_HERE, "libutv.so")
 
 UTV_OK, UTV_ERR_ARG, UTV_ERR_SHAPE, UTV_ERR_ALLOC, UTV_ERR_CUDA = 0, -1, -2, -3, -4
 UTV_ERR_NCCL, UTV_ERR_NUMERICAL, UTV_ERR_UNSUPPORTED = -5, -6, -7
-UTV_WANT_V, UTV_WANT_U, UTV_NULLIFY_T12, UTV_HOST_STREAMED, UTV_EXPLICIT_V = 1, 2, 4, 8, 16
+UTV_WANT_V, UTV_WANT_U, UTV_NULLIFY_T12, UTV_HOST_STREAMED, UTV_EXPLICIT_V, UTV_KEEP_FACTORS = 1, 2, 4, 8, 16, 32
 
 EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "utv_set_stream", "utv_synchronize",
             "utv_factor", "utv_solve", "utv_lstsq", "utv_version", "utv_sketch", "utv_philox", "utv_hqr",
             "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read",
             "utv_profile_dump", "utv_svd_block", "utv_svd_status", "utv_trsm_upper",
             "utv_rank_diag", "utv_set_device_budget", "utv_stream_stats", "utv_get_unique_id",
-            "utv_create_local_group", "utv_dist_local_cols"]
+            "utv_create_local_group", "utv_dist_local_cols", "utv_tune", "utv_solve_rhs"]
 PROF_FAMILIES = ["gemm", "panel", "svd", "sketch", "solve", "misc"]
 
 
@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
             "utv_create_local_group": ([p, C.c_int, p, p], st),
             "utv_dist_local_cols": ([i64, i64, C.c_int, C.c_int], i64),
             "utv_stream_stats": ([p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], st),
+            "utv_tune": ([C.c_int, i64, C.POINTER(i64)], st),
+            "utv_solve_rhs": ([p, i64, i64, i64, p, i64, p, i64, p, i64, C.POINTER(i64)], st),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -231,6 +233,19 @@ class Handle:
         o = opts.c()
         self.check(lib().utv_lstsq(self.h, m, n, k, _ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(X), _ld(X), C.byref(o),
                                    C.byref(r)))
+        return int(r.value)
+
+    def solve_rhs(self, T, B, X, m: int | None = None) -> int:
+        """X = V(:,0:r) T11^{-1} (U^T B)(0:r) for a NEW B with the factors kept by the last call with
+        UTV_KEEP_FACTORS (utv_solve_rhs); B is overwritten by U^T B.  T is the T that call left in A
+        (on a multi-GPU handle: this rank's shard).  Returns r."""
+        _check_f64(T, B, X)
+        k = B.shape[1] if B.dim() == 2 else 1
+        m = B.shape[0] if m is None else m
+        n = X.shape[0]
+        r = C.c_int64(-1)
+        self.check(lib().utv_solve_rhs(self.h, m, n, k, _ptr(T), _ld(T), _ptr(B), _ld(B), _ptr(X), _ld(X),
+                                       C.byref(r)))
         return int(r.value)
 
     def set_device_budget(self, nbytes: int):
@@ -390,6 +405,34 @@ def local_group(nranks: int, devices=None, streams=None) -> list:
     if st != UTV_OK:
         raise UtvError(st, "utv_create_local_group failed")
     return [Handle._wrap(C.c_void_p(hs[r]), devices[r], streams[r]) for r in range(nranks)]
+
+
+UTV_TUNE_GEMM_CFG, UTV_TUNE_GEMM_SPLITS, UTV_TUNE_GEMM_PATH, UTV_TUNE_QR_GLOBAL, UTV_TUNE_QR_CTAS = 1, 2, 3, 4, 5
+
+
+def tune(key: int, value: int) -> int:
+    """Set a process-wide implementation knob (utv_tune, include/utv_steps.h); returns the old value."""
+    old = C.c_int64(0)
+    st = lib().utv_tune(int(key), int(value), C.byref(old))
+    if st != UTV_OK:
+        raise UtvError(st, f"utv_tune: unknown key {key}")
+    return int(old.value)
+
+
+class tuned:
+    """Context manager: ``with tuned(UTV_TUNE_GEMM_CFG, 0): ...`` forces a knob and restores it."""
+
+    def __init__(self, *pairs):
+        self.pairs = [(pairs[i], pairs[i + 1]) for i in range(0, len(pairs), 2)]
+        self.old = []
+
+    def __enter__(self):
+        self.old = [(k, tune(k, v)) for k, v in self.pairs]
+        return self
+
+    def __exit__(self, *a):
+        for k, v in reversed(self.old):
+            tune(k, v)
 
 
 def dist_local_cols(n: int, block: int, nranks: int, rank: int) -> int:

@@ -664,11 +664,18 @@ void dispatch(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K
   else launch_t<true, true, VEC, ID>(st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, splits, kc, partial);
 }
 
-int g_force_wn = 0;   // 0 = heuristic; 1..3 forces a tile configuration (benchmarking)
+// Test / tuning knobs (utv_tune, include/utv_steps.h): -1 / 0 = automatic.
+int g_force_cfg = -1;      // tile configuration 0..5
+int g_force_splits = 0;    // split-K factor >= 1 (clamped to the workspace)
+int g_force_path = 0;      // 1 = the cp.async fallback kernel instead of TMA
 
 }  // namespace
 
-void dgemm_force_tile_width(int cfg) { g_force_wn = cfg; }
+void dgemm_force(int cfg, int splits, int path) {
+  g_force_cfg = cfg >= 0 && cfg < kNumShapes ? cfg : -1;
+  g_force_splits = splits > 0 ? splits : 0;
+  g_force_path = path;
+}
 
 // Launch plan: tile configuration and split-K factor from a small cost model (waves of CTAs x
 // per-tile time + the split-K reduce traffic).  Fixes wave quantisation: e.g. 782 tiles on 148
@@ -707,10 +714,18 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int num_sms, size_t work_
     return true;
   }();
   (void)env_read;
-  const int cfg = g_force_wn ? g_force_wn : (N <= 32 ? kNarrowCfg : (K <= 1024 ? g_cfg_short : g_cfg_long));
+  const bool forced = g_force_cfg >= 0;
+  const int cfg = forced ? g_force_cfg : (N <= 32 ? kNarrowCfg : (K <= 1024 ? g_cfg_short : g_cfg_long));
+  if (g_force_splits > 0) {
+    // forced split-K: as many splits as requested that the workspace holds (>= 1 k-tile each)
+    int64_t s = std::min<int64_t>(g_force_splits, (K + BK - 1) / BK);
+    while (s > 1 && (size_t)s * (size_t)M * (size_t)N > work_doubles) --s;
+    const int64_t kc = s <= 1 ? K : ((K + s - 1) / s + BK - 1) / BK * BK;
+    return Plan{cfg, (int)((K + kc - 1) / kc), kc};
+  }
   double t0 = 0.0;
   Plan p0 = plan_for(cfg, M, N, K, num_sms, work_doubles, &t0);
-  if (!g_force_wn && cfg == 0 && K > 1024) {
+  if (!forced && cfg == 0 && K > 1024) {
     // long K: the 64 x 64 / 3-CTA tile balances small and mid-size outputs better; it runs ~2%
     // below the 128 x 128 tile when both fill the machine
     double t5 = 0.0;
@@ -754,7 +769,7 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
     const char* e = std::getenv("UTV_GEMM_TMA");
     return !(e && e[0] == '0');
   }();
-  const bool tma_ok = use_tma && aligned && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31);
+  const bool tma_ok = use_tma && g_force_path != 1 && aligned && M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31);
   bool done = false;
   if (tma_ok) {
     switch (plan.cfg) {

@@ -12,7 +12,8 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
            int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* work,
            size_t work_doubles, int num_sms);
 
-void dgemm_force_tile_width(int wn);   // 0 = heuristic, 2 or 4 (benchmarking)
+// utv_tune knobs: cfg 0..5 (else automatic), splits >= 1 (else automatic), path 1 = cp.async kernel
+void dgemm_force(int cfg, int splits, int path);
 int dgemm_split_count(int64_t M, int64_t N, int64_t K, int num_sms);
 size_t dgemm_workspace_doubles(int64_t M, int64_t N, int64_t K, int num_sms);
 

@@ -25,6 +25,8 @@ struct PanelWork {
 // In place: P (rows x w) -> R (upper triangle), zeros strictly below; W (rows x w) the explicit
 // unit-lower Householder vectors; tau (w); T (w x w, upper, zeros below) with
 // Q = H_0 ... H_{w-1} = I - W T W^T.  Requires rows >= w.
+// utv_tune knobs: force the global-memory sub-panel kernel; cap the cooperative CTAs (0 = auto)
+void panel_force(int global_variant, int ctas);
 void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
               double* T, int64_t ldt, const PanelWork& pw);
 

@@ -309,6 +309,16 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
 
 }  // namespace
 
+namespace {
+int g_qr_force_global = 0;   // utv_tune(UTV_TUNE_QR_GLOBAL): the global-memory qr2 variant at any size
+int g_qr_ctas = 0;           // utv_tune(UTV_TUNE_QR_CTAS): cap on the cooperative CTAs (0 = automatic)
+}  // namespace
+
+void panel_force(int global_variant, int ctas) {
+  g_qr_force_global = global_variant ? 1 : 0;
+  g_qr_ctas = ctas > 0 ? ctas : 0;
+}
+
 void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
               double* T, int64_t ldt, const PanelWork& pw) {
   if (w <= 0) return;
@@ -318,17 +328,22 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
     const int64_t R = rows - jb;
     // one CTA (no grid barrier) up to 1024 rows; else ~256+ rows per CTA, at most one per SM
     static const int env_max = [] { const char* e = std::getenv("UTV_QR_MAXCTAS"); return e ? std::atoi(e) : 0; }();
-    const int gmax = env_max > 0 ? std::min(env_max, pw.num_sms) : std::min(pw.num_sms, 160);
+    const int cap = g_qr_ctas > 0 ? g_qr_ctas : env_max;
+    const int gmax = cap > 0 ? std::min(cap, pw.num_sms) : std::min(pw.num_sms, 160);
     int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (R + 255) / 256));
-    if ((R + G - 1) / G > SMEM_ROWS_MAX && env_max > 0) G = (int)std::min<int64_t>(pw.num_sms, (R + SMEM_ROWS_MAX - 1) / SMEM_ROWS_MAX);
+    // a CTA cap alone keeps the shared-memory variant (more CTAs if needed); forcing the global
+    // variant keeps G as chosen
+    if ((R + G - 1) / G > SMEM_ROWS_MAX && cap > 0 && !g_qr_force_global)
+      G = (int)std::min<int64_t>(pw.num_sms, (R + SMEM_ROWS_MAX - 1) / SMEM_ROWS_MAX);
     const int64_t Lr = (R + G - 1) / G;
-    const bool smem = Lr <= SMEM_ROWS_MAX;
+    const bool smem = Lr <= SMEM_ROWS_MAX && !g_qr_force_global;
     int64_t Rv = R; int nbv = nb; double* Pb = P + cm(jb, jb, ldp); double* Wb = W + cm(jb, jb, ldw);
     int64_t wtop = jb; double* taub = tau + jb; double* Tb = T + cm(jb, jb, ldt);
     void* args[] = {&Rv, &nbv, &Pb, (void*)&ldp, &Wb, (void*)&ldw, &wtop, &taub, &Tb, (void*)&ldt,
                     (void*)&pw.part, (void*)&pw.bar};
     {
       ProfScope prof(st, kProfPanel, 1, 2.0 * (double)R * nb * nb, 16.0 * (double)R * nb);
+      prof.shape(R, nb, G, smem ? 1 : 0);                 // tag: 1 = shared-memory variant
       static std::atomic<unsigned long long> attr{0};
       ensure_smem_attr(qr2_kernel<true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr);
       const size_t smem_bytes = smem ? (size_t)Lr * SROW * sizeof(double) : 0;

@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <nccl.h>             // types and constants only; the functions are resolved with dlsym
 
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -11,6 +12,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/utv.h"
@@ -28,7 +30,11 @@ using namespace utv;
 struct Comm {
   int nranks = 1, rank = 0;
   virtual ~Comm() {}
-  virtual void abort() {}          // a failing rank releases its peers (in-process groups)
+  virtual void abort() {}          // a failing rank releases its peers
+  // Wait for the stream (replaces cudaStreamSynchronize on the multi-GPU path): NCCL polls the
+  // communicator's asynchronous error state and gives up after a timeout, so that a rank whose
+  // peer died does not wait forever (the caller's error path then aborts the communicator).
+  virtual void wait(cudaStream_t st) { UTV_CUDA(cudaStreamSynchronize(st)); }
   virtual void allreduce(double* buf, size_t n, cudaStream_t st) = 0;
   virtual void bcast(double* buf, size_t n, int root, cudaStream_t st) = 0;
   virtual void allgather(const double* send, double* recv, size_t n, cudaStream_t st) = 0;
@@ -49,6 +55,8 @@ struct NcclApi {
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 const NcclApi* nccl_api() {
@@ -67,7 +75,10 @@ const NcclApi* nccl_api() {
     a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(l, "ncclBroadcast"));
     a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(l, "ncclAllGather"));
     a.errorString = reinterpret_cast<decltype(a.errorString)>(dlsym(l, "ncclGetErrorString"));
-    if (a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.broadcast && a.allGather && a.errorString)
+    a.commAbort = reinterpret_cast<decltype(a.commAbort)>(dlsym(l, "ncclCommAbort"));
+    a.commGetAsyncError = reinterpret_cast<decltype(a.commGetAsyncError)>(dlsym(l, "ncclCommGetAsyncError"));
+    if (a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.broadcast && a.allGather && a.errorString &&
+        a.commAbort && a.commGetAsyncError)
       api = a;
   });
   return api.lib ? &api : nullptr;
@@ -76,16 +87,51 @@ const NcclApi* nccl_api() {
 struct NcclComm : Comm {
   const NcclApi* api = nullptr;
   ncclComm_t comm = nullptr;
+  bool aborted = false;
   void check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) throw CommError{std::string(what) + ": " + api->errorString(r)};
   }
+  void live() {
+    if (aborted) throw CommError{"the NCCL communicator was aborted by an earlier failure; destroy the handle"};
+  }
+  // ncclCommAbort: ends this rank's in-flight NCCL kernels and connections (a peer blocked in a
+  // collective with this rank then sees an error or its own timeout instead of hanging).
+  void abort() override {
+    if (comm && !aborted) {
+      api->commAbort(comm);
+      comm = nullptr;
+      aborted = true;
+    }
+  }
+  void wait(cudaStream_t st) override {
+    live();
+    static const double limit = [] {
+      const char* e = std::getenv("UTV_COMM_TIMEOUT_S");
+      return e ? std::atof(e) : 3600.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int it = 0;; ++it) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e == cudaSuccess) return;
+      if (e != cudaErrorNotReady) throw CudaError{e, "cudaStreamQuery (multi-GPU wait)", __LINE__};
+      ncclResult_t ae = ncclSuccess;
+      if (api->commGetAsyncError(comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+        throw CommError{std::string("NCCL asynchronous error: ") + api->errorString(ae)};
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+        throw CommError{"timed out waiting for the peer ranks (UTV_COMM_TIMEOUT_S)"};
+      if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
   void allreduce(double* buf, size_t n, cudaStream_t st) override {
+    live();
     if (n) check(api->allReduce(buf, buf, n, ncclFloat64, ncclSum, comm, st), "ncclAllReduce");
   }
   void bcast(double* buf, size_t n, int root, cudaStream_t st) override {
+    live();
     if (n) check(api->broadcast(buf, buf, n, ncclFloat64, root, comm, st), "ncclBroadcast");
   }
   void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
+    live();
     if (n) check(api->allGather(send, recv, n, ncclFloat64, comm, st), "ncclAllGather");
   }
   ~NcclComm() override {
@@ -192,6 +238,36 @@ struct LocalComm : Comm {
   }
 };
 
+// Factored V (SURVEY 8(f) #4): instead of accumulating V explicitly (2 n^3 flops at square
+// shapes, 23% of the work at q = 2), keep every step's block reflector (W_V, T_V) and V_s:
+//   V = Q_1 Q_2 ... Q_s D_1 ... D_s   (D_i = V_s on block i commutes with Q_j, j > i: H5),
+// and apply it to [z; 0] in the solve.  Used by utv_lstsq (V is not an output there).
+struct FactoredV {
+  double* W;       // sum_i n'_i b doubles: W_V of step i at woff[i] (ld n'_i)
+  double* T;       // nsteps b^2: T_V of step i (ld b)
+  double* Vs;      // nsteps b^2: V_s of step i (ld b)
+  std::vector<size_t> woff;
+  std::vector<int64_t> j0, np;
+  std::vector<char> has_q;
+};
+
+// Kept factorization (UTV_KEEP_FACTORS, the reuse that v23t cannot offer,
+// P:1726-1728): the last factorization's U and V in factored form, so that utv_solve_rhs can
+// solve for a new right-hand side with the T left in the caller's A.
+//   U = Q_U,1 ... Q_U,s  blockdiag(U_s,i)     (U_s,i on block i commutes with Q_U,j, j > i)
+//   V = Q_V,1 ... Q_V,s  blockdiag(V_s,i)     (FactoredV)
+struct Kept {
+  bool valid = false;
+  bool dist = false;       // multi-GPU handle: T is block-cyclically sharded
+  int64_t m = 0, n = 0, b = 0, r = 0;
+  double* buf = nullptr; size_t buf_doubles = 0;
+  FactoredV fv;
+  double* Wu = nullptr;    // sum_i m'_i bw_i doubles: W_U of step i at uoff[i] (ld m'_i = m - j0_i)
+  double* Tu = nullptr;    // nsteps b^2: T_U of step i (ld b)
+  double* Us = nullptr;    // nsteps b^2: U_s of step i (ld b)
+  std::vector<size_t> uoff;
+};
+
 struct utv_handle_s {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -222,8 +298,12 @@ struct utv_handle_s {
   cudaEvent_t ev_loaded[kStg] = {}, ev_free[kStg] = {}, ev_done = nullptr, ev_wb = nullptr;
   // multi-GPU (utv_create_dist / utv_create_local_group)
   Comm* comm = nullptr;
+  double* agree = nullptr;       // device scratch of the multi-GPU argument agreement (2 doubles)
+  bool agreed_failure = false;   // the failing call was agreed on by every rank: no abort needed
+  bool collective_phase = false; // this call has entered the ranks' collectives (abort on failure)
   int coop_share = 1;            // ranks of an in-process group sharing this device (cooperative-CTA cap)
   double* dbuf = nullptr; size_t dbuf_doubles = 0;
+  Kept kept;                     // UTV_KEEP_FACTORS
   Profiler prof;
 };
 
@@ -247,10 +327,14 @@ utv_status guarded(utv_handle h, F&& f) {
       explicit ProfBind(Profiler* p) { g_prof = p; }
       ~ProfBind() { g_prof = nullptr; }
     } bind(h->prof.on ? &h->prof : nullptr);
+    h->agreed_failure = false;
+    h->collective_phase = false;
     try {
       f();
     } catch (...) {
-      if (h->comm) h->comm->abort();
+      // abort only once the ranks are inside the call's collectives (a failure before that is
+      // rank-local: no peer is waiting for this rank yet, or the ranks agreed on the failure)
+      if (h->comm && h->collective_phase && !h->agreed_failure) h->comm->abort();
       throw;
     }
     h->last_error.clear();
@@ -421,19 +505,6 @@ void copy2d(cudaStream_t st, void* dst, int64_t ldd, const void* src, int64_t ld
   UTV_CUDA(cudaMemcpy2DAsync(dst, (size_t)ldd * 8, src, (size_t)lds * 8, (size_t)rows * 8, (size_t)cols, kind, st));
 }
 
-// Factored V (SURVEY 8(f) #4): instead of accumulating V explicitly (2 n^3 flops at square
-// shapes, 23% of the work at q = 2), keep every step's block reflector (W_V, T_V) and V_s:
-//   V = Q_1 Q_2 ... Q_s D_1 ... D_s   (D_i = V_s on block i commutes with Q_j, j > i: H5),
-// and apply it to [z; 0] in the solve.  Used by utv_lstsq (V is not an output there).
-struct FactoredV {
-  double* W;       // sum_i n'_i b doubles: W_V of step i at woff[i] (ld n'_i)
-  double* T;       // nsteps b^2: T_V of step i (ld b)
-  double* Vs;      // nsteps b^2: V_s of step i (ld b)
-  std::vector<size_t> woff;
-  std::vector<int64_t> j0, np;
-  std::vector<char> has_q;
-};
-
 size_t factored_w_doubles(int64_t n, int64_t b) {
   size_t tot = 0;
   for (int64_t j0 = 0; j0 < n; j0 += b)
@@ -441,9 +512,57 @@ size_t factored_w_doubles(int64_t n, int64_t b) {
   return tot;
 }
 
+size_t kept_u_doubles(int64_t m, int64_t n, int64_t b) {
+  size_t tot = 0;
+  for (int64_t j0 = 0; j0 < n; j0 += b) tot += (size_t)(m - j0) * (size_t)std::min(b, n - j0);
+  return tot;
+}
+
+// Allocate the kept-factor store (UTV_KEEP_FACTORS) for an m x n factorization with block b.
+Kept& kept_prepare(utv_handle h, int64_t m, int64_t n, int64_t b, bool dist) {
+  Kept& kp = h->kept;
+  kp.valid = false;
+  const int64_t nsteps = (n + b - 1) / b;
+  const size_t wdbl = factored_w_doubles(n, b), tdbl = (size_t)nsteps * b * b, udbl = kept_u_doubles(m, n, b);
+  ensure_buf(&kp.buf, &kp.buf_doubles, wdbl + 4 * tdbl + udbl + 64);
+  kp.fv = FactoredV{};
+  kp.fv.W = kp.buf; kp.fv.T = kp.buf + wdbl; kp.fv.Vs = kp.fv.T + tdbl;
+  kp.Tu = kp.fv.Vs + tdbl; kp.Us = kp.Tu + tdbl; kp.Wu = kp.Us + tdbl;
+  kp.uoff.clear();
+  kp.m = m; kp.n = n; kp.b = b; kp.r = 0; kp.dist = dist;
+  return kp;
+}
+
+// Record step `step`'s W_U (mp x bw at Wu, ld ldwu) and T_U (ld b) in the kept store.
+void kept_push_u(cudaStream_t st, Kept& kp, int64_t step, int64_t mp, int64_t bw, const double* Wu, int64_t ldwu,
+                 const double* Tu) {
+  const size_t off = kp.uoff.empty() ? 0 : kp.uoff.back() + (size_t)(kp.m - (step - 1) * kp.b) * kp.b;
+  kp.uoff.push_back(off);
+  launch_copy(st, mp, bw, Wu, ldwu, kp.Wu + off, mp);
+  launch_copy(st, bw, bw, Tu, kp.b, kp.Tu + (size_t)step * kp.b * kp.b, kp.b);
+}
+
+// C := U^T C with the kept factors, step by step as in the factorization: Q_U,i^T on rows j0:m,
+// then U_s,i^T on rows j0:j0+bw (C m x k, device, ldc).
+void kept_apply_ut(const Ctx& c, const Kept& kp, double* Cm, int64_t ldc, int64_t k) {
+  double *Z1 = c.at(c.L.Z1), *Z2 = c.at(c.L.Z2);
+  const int64_t m = kp.m, n = kp.n, b = kp.b;
+  for (int64_t j0 = 0, i = 0; j0 < n; j0 += b, ++i) {
+    const int64_t bw = std::min(b, n - j0), mp = m - j0;
+    const double* W = kp.Wu + kp.uoff[i];
+    double* Cr = Cm + j0;
+    c.gemm(true, false, bw, k, mp, 1.0, W, mp, Cr, ldc, 0.0, Z1, bw);
+    c.gemm(true, false, bw, k, bw, 1.0, kp.Tu + (size_t)i * b * b, b, Z1, bw, 0.0, Z2, bw);
+    c.gemm(false, false, mp, k, bw, -1.0, W, mp, Z2, bw, 1.0, Cr, ldc);
+    c.gemm(true, false, bw, k, bw, 1.0, kp.Us + (size_t)i * b * b, b, Cr, ldc, 0.0, Z1, bw);
+    launch_copy(c.st, bw, k, Z1, bw, Cr, ldc);
+  }
+}
+
 // The randUTV factorization on device buffers (fig:alg_utv).
 void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, double* V, int64_t ldv, double* U,
-                 int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts& o, FactoredV* fv = nullptr) {
+                 int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts& o, FactoredV* fv = nullptr,
+                 Kept* kp = nullptr) {
   cudaStream_t st = c.st;
   const Layout& L = c.L;
   const int64_t b = o.block;
@@ -463,7 +582,7 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
   bool svd_pending = false;
   bool us_pending = false, us_applied = false;      // deferred A12 := U_s^T A12 (see below)
   int64_t us_j0 = 0, us_bw = 0;
-  int us_buf = 0;
+  const double* us_ptr = nullptr;                   // U_s of the pending A12 update
   // the side stream must not start before the work enqueued on the main stream so far
   UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
   UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
@@ -510,6 +629,7 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     }
     // ---- apply transformations from the left ----
     panel_qr(st, mp, bw, Ap, lda, Wu, m, tauu, Tu, b, c.pw);                            // a5 (+R13)
+    if (kp) kept_push_u(st, *kp, step, mp, bw, Wu, m, Tu);                              // keep W_U, T_U
     if (nr > 0) {                                                                       // a6, R3
       double* Ar = A + cm(j0, j0 + bw, lda);
       c.gemm(true, false, bw, nr, mp, 1.0, Wu, m, Ar, lda, 0.0, Z1, bw);              // W_U^T A_r
@@ -544,8 +664,7 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     if (us_pending) {
       UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
       double* A12p = A + cm(us_j0, us_j0 + us_bw, lda);
-      const double* Usp = (us_buf ? c.at(L.Us2) : c.at(L.Us));
-      c.gemm(true, false, us_bw, n - us_j0 - us_bw, us_bw, 1.0, Usp, b, A12p, lda, 0.0, c.at(L.tmp), us_bw);
+      c.gemm(true, false, us_bw, n - us_j0 - us_bw, us_bw, 1.0, us_ptr, b, A12p, lda, 0.0, c.at(L.tmp), us_bw);
       launch_copy(st, us_bw, n - us_j0 - us_bw, c.at(L.tmp), us_bw, A12p, lda);
       UTV_CUDA(cudaEventRecord(c.h->ev_us, st));
       us_pending = false;
@@ -559,7 +678,8 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
     UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
     double* Vsi = fv ? fv->Vs + (size_t)step * b * b : Vs;                             // V_s (kept if factored)
-    double* Usi = (step & 1) ? c.at(L.Us2) : Us;                                        // kept until applied
+    double* Usi = kp ? kp->Us + (size_t)step * b * b                                   // kept until applied
+                     : ((step & 1) ? c.at(L.Us2) : Us);
     svd_small(sd, bw, Ap, lda, Usi, b, sig, Vsi, b, c.sw);                             // a7
     launch_set_diag(sd, bw, sig, Ap, lda);
     if (j0 > 0) {                                                                       // A01 := A01 V_s
@@ -571,7 +691,7 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     }
     if (nr > 0) {                                                                       // A12 := U_s^T A12
       us_pending = true;                                                                // next step, main
-      us_j0 = j0; us_bw = bw; us_buf = (int)(step & 1);
+      us_j0 = j0; us_bw = bw; us_ptr = Usi;
     }
     if (V) {                                                                            // V1 := V1 V_s
       double* V1 = V + cm(0, j0, ldv);
@@ -594,8 +714,7 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
   if (svd_pending) UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
   if (us_pending) {                                                                     // the last A12
     double* A12p = A + cm(us_j0, us_j0 + us_bw, lda);
-    const double* Usp = (us_buf ? c.at(L.Us2) : c.at(L.Us));
-    c.gemm(true, false, us_bw, n - us_j0 - us_bw, us_bw, 1.0, Usp, b, A12p, lda, 0.0, c.at(L.tmp), us_bw);
+    c.gemm(true, false, us_bw, n - us_j0 - us_bw, us_bw, 1.0, us_ptr, b, A12p, lda, 0.0, c.at(L.tmp), us_bw);
     launch_copy(st, us_bw, n - us_j0 - us_bw, c.at(L.tmp), us_bw, A12p, lda);
   }
   if (m > n) launch_set_zero(st, m - n, n, A + n, lda);   // rows below T (already 0 by R13; kept explicit)
@@ -610,7 +729,8 @@ int64_t finish_factor(const Ctx& c, int64_t n, const double* T, int64_t ldt, dou
   }
   UTV_CUDA(cudaMemcpyAsync(c.h->h_info, c.h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   UTV_CUDA(cudaMemcpyAsync(c.h->h_info + 2, c.h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  UTV_CUDA(cudaStreamSynchronize(st));
+  if (c.h->comm) c.h->comm->wait(st);
+  else UTV_CUDA(cudaStreamSynchronize(st));
   if (c.h->h_info[2]) fail(UTV_ERR_NUMERICAL, "NaN or Inf in A or B");
   if (c.h->h_info[1]) fail(UTV_ERR_NUMERICAL, "Jacobi SVD of a diagonal block did not converge in 30 sweeps");
   return want_rank ? *c.h->h_rank : -1;
@@ -907,6 +1027,8 @@ void factor_ooc(const Ctx& c, Ooc& o, double* Cd, int64_t ldc, int64_t k, const 
     const int buf = (int)(step & 1);
     int64_t lda_i = m;
     double* Ai = ooc_block(o, c, j0, bw, m, &lda_i, buf);
+    // n <= b: no sketch pass ran, so a streamed block 0 has not been checked for NaN / Inf yet
+    if (step == 0 && !right && j0 < o.c_res) launch_check_finite(st, m, bw, Ai, lda_i, c.h->flag);
     if (right) c.gemm(false, true, m, bw, b, -1.0, X2, m, WV, np, 1.0, Ai, lda_i);
     if (fin_pending) {
       UTV_CUDA(cudaStreamWaitEvent(st, c.h->ev_svd, 0));
@@ -1149,28 +1271,98 @@ int64_t dist_local_cols(int64_t n, int64_t b, int P, int p) {
   return c;
 }
 
+size_t dist_dbuf_doubles(int64_t n, int64_t b, int P, int64_t k) {
+  const int64_t nb = (n + b - 1) / b, Lmax = (nb + P - 1) / P * b;
+  return (size_t)Lmax * b * (P + 1) + n + 64 + 2 * (size_t)b * (size_t)std::max<int64_t>(k, 1) + 64;
+}
+
+// Every device allocation lstsq_dist makes, done up front (before the ranks agree on the call).
+void dist_reserve(utv_handle h, int64_t m, int64_t n, int64_t k, const utv_opts& opt) {
+  const int64_t b = opt.block, nsteps = (n + b - 1) / b;
+  make_ctx(h, m, n, k, b);
+  if (opt.flags & UTV_KEEP_FACTORS) {
+    kept_prepare(h, m, n, b, true);
+  } else {
+    ensure_buf(&h->vbuf, &h->vbuf_doubles, factored_w_doubles(n, b) + 2 * (size_t)nsteps * b * b + 64);
+  }
+  ensure_buf(&h->dbuf, &h->dbuf_doubles, dist_dbuf_doubles(n, b, h->comm->nranks, k));
+}
+
+// The ranks of a multi-GPU handle agree on a call before its first collective: one AllReduce of
+// "this rank failed its checks".  Any failure fails the call on every rank (no abort needed: no
+// collective of the method was started, so the communicator stays usable).
+void dist_agree(utv_handle h, utv_status local, const std::string& msg) {
+  cudaStream_t st = h->stream;
+  const double v = local != UTV_OK ? 1.0 : 0.0;
+  double sum = 0.0;
+  h->collective_phase = true;
+  UTV_CUDA(cudaMemcpyAsync(h->agree, &v, sizeof(double), cudaMemcpyHostToDevice, st));
+  h->comm->allreduce(h->agree, 1, st);
+  UTV_CUDA(cudaMemcpyAsync(&sum, h->agree, sizeof(double), cudaMemcpyDeviceToHost, st));
+  h->comm->wait(st);
+  if (local != UTV_OK) { h->agreed_failure = true; fail(local, msg); }
+  if (sum != 0.0) {
+    h->agreed_failure = true;
+    fail(UTV_ERR_ARG, "the call was rejected on " + std::to_string((int)sum) + " peer rank(s) (argument or "
+                      "allocation error there); nothing was computed");
+  }
+}
+
+// a9 on a block-cyclic T: z = T11^{-1} C(0:r, :) into the zsolve buffer (ld r), block by block from
+// the bottom: one AllReduce of the partial sums T_{blk, >blk} z and one Broadcast of z_blk (from the
+// block's owner) per block.  A = this rank's shard of T (lda), C replicated (ldc).
+void dist_solve_z(const Ctx& c, Comm& comm, int64_t r, int64_t b, const double* A, int64_t lda, const double* Cm,
+                  int64_t ldc, int64_t k) {
+  if (r <= 0 || k <= 0) return;
+  cudaStream_t st = c.st;
+  const int P = comm.nranks, p = comm.rank;
+  double* Zb = c.at(c.L.zsolve);
+  double* Sp = c.at(c.L.nY);                                                             // my partial sums
+  double* D = c.at(c.L.R);
+  double* sbuf = c.at(c.L.tmp);                                                          // b x k
+  double* zb = c.at(c.L.tmp2);                                                           // b x k
+  launch_set_zero(st, r, k, Sp, r);
+  for (int64_t blk = (r - 1) / b; blk >= 0; --blk) {
+    const int64_t j0 = blk * b, j1 = std::min(r, j0 + b), w = j1 - j0;
+    const int o = (int)(blk % P);
+    launch_copy(st, w, k, Sp + j0, r, sbuf, w);
+    comm.allreduce(sbuf, (size_t)w * k, st);                                             // sum_l T_blk,l z_l
+    if (p == o) {
+      const int64_t lc = (blk / P) * b;
+      launch_copy(st, w, k, Cm + j0, ldc, zb, w);
+      launch_axpy(st, w * k, -1.0, sbuf, zb);
+      launch_copy(st, w, w, A + cm(j0, lc, lda), lda, D, b);
+      launch_trsv_block(st, 0, w, D, b, zb, w, k);
+      if (j0 > 0) c.gemm(false, false, j0, k, w, 1.0, A + cm(0, lc, lda), lda, zb, w, 1.0, Sp, r);
+    }
+    comm.bcast(zb, (size_t)w * k, o, st);
+    launch_copy(st, w, k, zb, w, Zb + j0, r);
+  }
+}
+
 int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
                    double* X, int64_t ldx, const utv_opts& opt) {
   Comm& comm = *h->comm;
   const int P = comm.nranks, p = comm.rank;
   const int64_t b = opt.block, nb = (n + b - 1) / b;
   const int64_t nloc = dist_local_cols(n, b, P, p);
-  if (opt.flags & (UTV_NULLIFY_T12 | UTV_EXPLICIT_V | UTV_HOST_STREAMED))
-    fail(UTV_ERR_UNSUPPORTED, "the multi-GPU path implements the fast option with factored V only");
-  if ((nloc > 0 && !is_device_ptr(A)) || (k > 0 && (!is_device_ptr(B) || !is_device_ptr(X))))
-    fail(UTV_ERR_ARG, "the multi-GPU path takes device pointers (A = this rank's shard)");
   cudaStream_t st = h->stream;
   const int ns = h->num_sms;
   Ctx c = make_ctx(h, m, n, k, b);
   const Layout& L = c.L;
   const int64_t nsteps = nb;
   const size_t wdbl = factored_w_doubles(n, b), tdbl = (size_t)nsteps * b * b;
-  ensure_buf(&h->vbuf, &h->vbuf_doubles, wdbl + 2 * tdbl + 64);
-  FactoredV fv;
-  fv.W = h->vbuf; fv.T = h->vbuf + wdbl; fv.Vs = fv.T + tdbl;
+  const bool keep = (opt.flags & UTV_KEEP_FACTORS) != 0;
+  Kept* kp = keep ? &kept_prepare(h, m, n, b, true) : nullptr;
+  FactoredV fv_local;
+  if (!keep) {
+    ensure_buf(&h->vbuf, &h->vbuf_doubles, wdbl + 2 * tdbl + 64);
+    fv_local.W = h->vbuf; fv_local.T = h->vbuf + wdbl; fv_local.Vs = fv_local.T + tdbl;
+  }
+  FactoredV& fv = keep ? kp->fv : fv_local;
   const int64_t Lmax = (nb + P - 1) / P * b;
   const size_t kk = (size_t)std::max<int64_t>(k, 1);
-  ensure_buf(&h->dbuf, &h->dbuf_doubles, (size_t)Lmax * b * (P + 1) + n + 64 + 2 * (size_t)b * kk + 64);
+  ensure_buf(&h->dbuf, &h->dbuf_doubles, dist_dbuf_doubles(n, b, P, k));
   double* Ypad = h->dbuf;
   double* recv = Ypad + (size_t)Lmax * b;
   double* dg = recv + (size_t)P * Lmax * b;
@@ -1191,7 +1383,7 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   auto apply_pending = [&]() {
     if (!pend) return;
     if (p == p_owner) UTV_CUDA(cudaStreamWaitEvent(st, h->ev_svd, 0));
-    double* Usp = (p_i & 1) ? c.at(L.Us2) : Us;
+    double* Usp = kp ? kp->Us + (size_t)p_i * b * b : ((p_i & 1) ? c.at(L.Us2) : Us);
     double* sgp = (p_i & 1) ? c.at(L.sig2) : sig;
     double* Vsp = fv.Vs + (size_t)p_i * b * b;
     comm.bcast(Usp, (size_t)b * b, p_owner, st);
@@ -1251,6 +1443,7 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
     if (own) panel_qr(st, mp, bw, At, lda, Wu, m, tauu, Tu, b, c.pw);                   // a5
     comm.bcast(LU + cm(0, b, m), (size_t)m * b, owner, st);
     comm.bcast(Tu, (size_t)b * b, owner, st);
+    if (kp) kept_push_u(st, *kp, i, mp, bw, Wu, m, Tu);                                  // keep W_U, T_U
     if (nrl > 0) {                                                                      // a6, R3
       double* Ar = A + cm(j0, lr, lda);
       c.gemm(true, false, bw, nrl, mp, 1.0, Wu, m, Ar, lda, 0.0, Z1, bw);
@@ -1278,7 +1471,7 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
     apply_pending();
     if (own) {
       double* Vsi = fv.Vs + (size_t)i * b * b;
-      double* Usi = (i & 1) ? c.at(L.Us2) : Us;
+      double* Usi = kp ? kp->Us + (size_t)i * b * b : ((i & 1) ? c.at(L.Us2) : Us);
       double* sgi = (i & 1) ? c.at(L.sig2) : sig;
       UTV_CUDA(cudaEventRecord(h->ev_panel, st));
       UTV_CUDA(cudaStreamWaitEvent(c.side, h->ev_panel, 0));
@@ -1298,40 +1491,22 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   // every rank fails alike: AllReduce the local NaN / Jacobi flags
   UTV_CUDA(cudaMemcpyAsync(h->h_info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   UTV_CUDA(cudaMemcpyAsync(h->h_info + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  UTV_CUDA(cudaStreamSynchronize(st));
+  comm.wait(st);
   const double fl[2] = {(double)h->h_info[2], (double)h->h_info[1]};
   UTV_CUDA(cudaMemcpyAsync(flags, fl, sizeof(fl), cudaMemcpyHostToDevice, st));
   comm.allreduce(flags, 2, st);
   double flo[2] = {0.0, 0.0};
   UTV_CUDA(cudaMemcpyAsync(flo, flags, sizeof(flo), cudaMemcpyDeviceToHost, st));
-  UTV_CUDA(cudaStreamSynchronize(st));
+  comm.wait(st);
+  h->agreed_failure = flo[0] != 0.0 || flo[1] != 0.0;                                    // every rank fails alike
   if (flo[0] != 0.0) fail(UTV_ERR_NUMERICAL, "NaN or Inf in A or B (on some rank)");
   if (flo[1] != 0.0) fail(UTV_ERR_NUMERICAL, "Jacobi SVD of a diagonal block did not converge in 30 sweeps");
   const int64_t r = finish_factor(c, n, dg, 0, opt.tau, true);                          // a8 (replicated)
+  if (kp) { kp->r = r; kp->valid = true; }
   if (k <= 0) return r;
-  // a9: z = T11^{-1} C(0:r, :) block by block from the bottom
-  double* Zb = c.at(L.zsolve);
-  double* Sp = c.at(L.nY);                                                               // my partial sums
-  double* D = c.at(L.R);
-  if (r > 0) launch_set_zero(st, r, k, Sp, r);
-  for (int64_t blk = r > 0 ? (r - 1) / b : -1; blk >= 0; --blk) {
-    const int64_t j0 = blk * b, j1 = std::min(r, j0 + b), w = j1 - j0;
-    const int o = (int)(blk % P);
-    launch_copy(st, w, k, Sp + j0, r, sbuf, w);
-    comm.allreduce(sbuf, (size_t)w * k, st);                                             // sum_l T_blk,l z_l
-    if (p == o) {
-      const int64_t lc = (blk / P) * b;
-      launch_copy(st, w, k, B + j0, ldb, zb, w);
-      launch_axpy(st, w * k, -1.0, sbuf, zb);
-      launch_copy(st, w, w, A + cm(j0, lc, lda), lda, D, b);
-      launch_trsv_block(st, 0, w, D, b, zb, w, k);
-      if (j0 > 0) c.gemm(false, false, j0, k, w, 1.0, A + cm(0, lc, lda), lda, zb, w, 1.0, Sp, r);
-    }
-    comm.bcast(zb, (size_t)w * k, o, st);
-    launch_copy(st, w, k, zb, w, Zb + j0, r);
-  }
+  dist_solve_z(c, comm, r, b, A, lda, B, ldb, k);                                        // a9
   solve_factored(c, n, r, nullptr, 0, nullptr, 0, k, X, ldx, fv, b, nullptr, true);      // X = V z (replicated)
-  UTV_CUDA(cudaStreamSynchronize(st));
+  comm.wait(st);
   return r;
 }
 
@@ -1372,6 +1547,7 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_us, cudaEventDisableTiming));
     UTV_CUDA(cudaMalloc((void**)&h->info, 64 * sizeof(int)));
     UTV_CUDA(cudaMalloc((void**)&h->flag, sizeof(int)));
+    UTV_CUDA(cudaMalloc((void**)&h->agree, 2 * sizeof(double)));
     UTV_CUDA(cudaMalloc((void**)&h->d_rank, sizeof(int64_t)));
     UTV_CUDA(cudaMallocHost((void**)&h->h_rank, sizeof(int64_t)));
     UTV_CUDA(cudaMallocHost((void**)&h->h_info, 4 * sizeof(int)));
@@ -1469,8 +1645,8 @@ utv_status utv_destroy(utv_handle h) {
   cudaFree(h->dbuf);
   delete h->comm;
   cudaFree(h->bar2);
-  cudaFree(h->ws); cudaFree(h->bar); cudaFree(h->info); cudaFree(h->flag); cudaFree(h->d_rank);
-  cudaFree(h->vbuf); cudaFree(h->stage); cudaFree(h->nbuf);
+  cudaFree(h->ws); cudaFree(h->bar); cudaFree(h->info); cudaFree(h->flag); cudaFree(h->d_rank); cudaFree(h->agree);
+  cudaFree(h->vbuf); cudaFree(h->stage); cudaFree(h->nbuf); cudaFree(h->kept.buf);
   cudaFreeHost(h->h_rank); cudaFreeHost(h->h_info);
   cudaGetLastError();
   delete h;
@@ -1500,11 +1676,17 @@ utv_status utv_factor(utv_handle h, int64_t m, int64_t n, double* A, int64_t lda
     const bool want_u = U && (opts->flags & UTV_WANT_U);
     if (want_u) check_ld("ldu", ldu, m);
     if (B && k > 0) check_ld("ldb", ldb, m);
-    if (n == 0) { if (rank) *rank = 0; return; }
-    Ctx c = make_ctx(h, m, n, k, opts->block);
-    factor_impl(c, m, n, A, lda, V, ldv, want_u ? U : nullptr, ldu, (B && k > 0) ? B : nullptr, ldb, k, *opts);
     const bool nullify = (opts->flags & UTV_NULLIFY_T12) != 0;
-    int64_t r = finish_factor(c, n, A, lda, opts->tau, rank != nullptr || nullify);
+    const bool keep = (opts->flags & UTV_KEEP_FACTORS) != 0;
+    if (keep && nullify) fail(UTV_ERR_UNSUPPORTED, "UTV_KEEP_FACTORS with UTV_NULLIFY_T12");
+    if (keep && !is_device_ptr(A)) fail(UTV_ERR_UNSUPPORTED, "UTV_KEEP_FACTORS needs A in device memory");
+    if (n == 0) { if (rank) *rank = 0; return; }
+    Kept* kp = keep ? &kept_prepare(h, m, n, opts->block, false) : nullptr;
+    Ctx c = make_ctx(h, m, n, k, opts->block);
+    factor_impl(c, m, n, A, lda, V, ldv, want_u ? U : nullptr, ldu, (B && k > 0) ? B : nullptr, ldb, k, *opts,
+                kp ? &kp->fv : nullptr, kp);
+    int64_t r = finish_factor(c, n, A, lda, opts->tau, rank != nullptr || nullify || keep);
+    if (kp) { kp->r = r; kp->valid = true; }
     if (nullify) nullify_impl(c, n, r, A, lda, V, ldv, opts->block, nullptr);   // fig:alg_axb line 3
     if (rank) *rank = r;
   });
@@ -1520,6 +1702,51 @@ utv_status utv_solve(utv_handle h, int64_t m, int64_t n, int64_t r, const double
     if (!X || (r > 0 && (!T || !V || !C))) fail(UTV_ERR_ARG, "NULL matrix");
     Ctx c = make_ctx(h, m, n, k, 1);
     solve_impl(c, n, r, T, ldt, V, ldv, C, ldc, k, X, ldx);
+  });
+}
+
+utv_status utv_solve_rhs(utv_handle h, int64_t m, int64_t n, int64_t k, const double* T, int64_t ldt, double* B,
+                         int64_t ldb, double* X, int64_t ldx, int64_t* rank) {
+  return guarded(h, [&] {
+    Kept& kp = h->kept;
+    utv_status local = UTV_OK;
+    std::string msg;
+    try {
+      if (!kp.valid) fail(UTV_ERR_ARG, "no kept factorization: factor with UTV_KEEP_FACTORS first");
+      if (m != kp.m || n != kp.n) fail(UTV_ERR_SHAPE, "m, n differ from the kept factorization");
+      if (k < 0) fail(UTV_ERR_ARG, "k < 0");
+      if (k > 0) {
+        check_ld("ldb", ldb, m); check_ld("ldx", ldx, n);
+        if (kp.dist) {
+          if (!h->comm) fail(UTV_ERR_ARG, "the kept factorization is a multi-GPU one");
+          const int64_t nloc = dist_local_cols(n, kp.b, h->comm->nranks, h->comm->rank);
+          if (nloc > 0) check_ld("ldt", ldt, m);
+          if (!B || !X || (nloc > 0 && kp.r > 0 && !T)) fail(UTV_ERR_ARG, "NULL matrix");
+        } else {
+          check_ld("ldt", ldt, m);
+          if (!B || !X || (kp.r > 0 && !T)) fail(UTV_ERR_ARG, "NULL matrix");
+        }
+        if (!is_device_ptr(B) || !is_device_ptr(X) || (T && !is_device_ptr(T)))
+          fail(UTV_ERR_ARG, "utv_solve_rhs takes device pointers");
+        make_ctx(h, m, n, k, kp.b);                                    // reserve the workspace
+      }
+    } catch (const ApiError& e) {
+      local = e.st;
+      msg = e.msg;
+    }
+    if (h->comm) dist_agree(h, local, msg);                            // multi-GPU: agree first
+    else if (local != UTV_OK) fail(local, msg);
+    const int64_t r = kp.r;
+    if (rank) *rank = r;
+    if (k == 0) return;
+    Ctx c = make_ctx(h, m, n, k, kp.b);
+    kept_apply_ut(c, kp, B, ldb, k);                                                    // C = U^T B
+    if (!kp.dist) {
+      solve_factored(c, n, r, T, ldt, B, ldb, k, X, ldx, kp.fv, kp.b);                 // a9
+    } else {
+      dist_solve_z(c, *h->comm, r, kp.b, T, ldt, B, ldb, k);
+      solve_factored(c, n, r, nullptr, 0, nullptr, 0, k, X, ldx, kp.fv, kp.b, nullptr, true);
+    }
   });
 }
 
@@ -1580,22 +1807,45 @@ int64_t lstsq_wide(utv_handle h, int64_t m, int64_t n, int64_t k, const double* 
 utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
                      double* X, int64_t ldx, const utv_opts* opts, int64_t* rank) {
   return guarded(h, [&] {
-    check_opts(opts);
-    if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
-    const bool wide = m < n;
-    if (wide && (h->comm || (opts->flags & UTV_HOST_STREAMED)))
-      fail(UTV_ERR_SHAPE, "m < n: single-GPU in-core utv_lstsq only (R21)");
-    if (wide && (opts->flags & UTV_NULLIFY_T12)) fail(UTV_ERR_UNSUPPORTED, "m < n with UTV_NULLIFY_T12");
-    check_ld("lda", lda, m);
-    if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
     if (h->comm) {                                                     // multi-GPU handle
-      const int64_t nloc = n > 0 ? dist_local_cols(n, opts->block, h->comm->nranks, h->comm->rank) : 0;
-      if ((nloc > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
+      // Every rank validates its arguments and reserves its device memory, then the ranks agree
+      // (one AllReduce of a flag) before the first collective of the method: a rank-local error
+      // fails the call on every rank instead of leaving the peers blocked in a collective.
+      utv_status local = UTV_OK;
+      std::string msg;
+      try {
+        check_opts(opts);
+        if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
+        if (m < n) fail(UTV_ERR_SHAPE, "m < n: single-GPU in-core utv_lstsq only (R21)");
+        if (opts->flags & (UTV_NULLIFY_T12 | UTV_EXPLICIT_V | UTV_HOST_STREAMED))
+          fail(UTV_ERR_UNSUPPORTED, "the multi-GPU path implements the fast option with factored V only");
+        check_ld("lda", lda, m);
+        if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
+        const int64_t nloc = n > 0 ? dist_local_cols(n, opts->block, h->comm->nranks, h->comm->rank) : 0;
+        if ((nloc > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
+        if ((nloc > 0 && !is_device_ptr(A)) || (k > 0 && (!is_device_ptr(B) || !is_device_ptr(X))))
+          fail(UTV_ERR_ARG, "the multi-GPU path takes device pointers (A = this rank's shard)");
+        if (n > 0) dist_reserve(h, m, n, k, *opts);
+      } catch (const ApiError& e) {
+        local = e.st;
+        msg = e.msg;
+      }
+      dist_agree(h, local, msg);
       if (n == 0) { if (rank) *rank = 0; return; }
       const int64_t r = lstsq_dist(h, m, n, k, A, lda, B, ldb, X, ldx, *opts);
       if (rank) *rank = r;
       return;
     }
+    check_opts(opts);
+    if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
+    const bool wide = m < n;
+    if (wide && (opts->flags & UTV_HOST_STREAMED)) fail(UTV_ERR_SHAPE, "m < n: single-GPU in-core utv_lstsq only (R21)");
+    if (wide && (opts->flags & UTV_NULLIFY_T12)) fail(UTV_ERR_UNSUPPORTED, "m < n with UTV_NULLIFY_T12");
+    check_ld("lda", lda, m);
+    if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
+    const bool keep = (opts->flags & UTV_KEEP_FACTORS) != 0;
+    if (keep && (wide || (opts->flags & (UTV_NULLIFY_T12 | UTV_HOST_STREAMED)) || (n > 0 && !is_device_ptr(A))))
+      fail(UTV_ERR_UNSUPPORTED, "UTV_KEEP_FACTORS: device A, m >= n, in core, without UTV_NULLIFY_T12");
     if ((n > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
     if (n == 0) { if (rank) *rank = 0; return; }
     if (opts->flags & UTV_HOST_STREAMED) {
@@ -1625,22 +1875,25 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
     }
     const bool explicit_v = (opts->flags & UTV_EXPLICIT_V) != 0;
     const bool nullify = (opts->flags & UTV_NULLIFY_T12) != 0;
-    FactoredV fv;
+    FactoredV fv_local;
     NullStore ns;
-    if (explicit_v) {
-      ensure_buf(&h->vbuf, &h->vbuf_doubles, (size_t)n * n);
-    } else {
+    Kept* kp = keep ? &kept_prepare(h, m, n, b, false) : nullptr;
+    if (explicit_v) ensure_buf(&h->vbuf, &h->vbuf_doubles, (size_t)n * n);
+    if (!explicit_v && !keep) {
       const int64_t nsteps = (n + b - 1) / b;
       const size_t wdbl = factored_w_doubles(n, b), tdbl = (size_t)nsteps * b * b;
       ensure_buf(&h->vbuf, &h->vbuf_doubles, wdbl + 2 * tdbl + 64);
-      fv.W = h->vbuf; fv.T = h->vbuf + wdbl; fv.Vs = fv.T + tdbl;
+      fv_local.W = h->vbuf; fv_local.T = h->vbuf + wdbl; fv_local.Vs = fv_local.T + tdbl;
     }
+    FactoredV& fv = keep ? kp->fv : fv_local;
     Ctx c = make_ctx(h, m, n, k, b);
     if (explicit_v)
-      factor_impl(c, m, n, dA, dlda, h->vbuf, n, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts);
+      factor_impl(c, m, n, dA, dlda, h->vbuf, n, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts,
+                  keep ? &fv : nullptr, kp);
     else
-      factor_impl(c, m, n, dA, dlda, nullptr, 0, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts, &fv);
+      factor_impl(c, m, n, dA, dlda, nullptr, 0, nullptr, 0, k > 0 ? dB : nullptr, dldb, k, *opts, &fv, kp);
     int64_t r = finish_factor(c, n, dA, dlda, opts->tau, true);
+    if (kp) { kp->r = r; kp->valid = true; }
     if (nullify) {                                                     // fig:alg_axb line 3
       if (!explicit_v) {
         ensure_buf(&h->nbuf, &h->nbuf_doubles, null_store_doubles(n, r, b) + 64);
@@ -1785,6 +2038,20 @@ utv_status utv_rank(utv_handle h, int64_t n, const double* T, int64_t ldt, doubl
     UTV_CUDA(cudaStreamSynchronize(h->stream));
     *rank = *h->h_rank;
   });
+}
+
+utv_status utv_tune(int key, int64_t value, int64_t* old) {
+  static std::mutex mu;
+  static int64_t cur[6] = {0, -1, 0, 0, 0, 0};
+  std::lock_guard<std::mutex> lk(mu);
+  if (key < UTV_TUNE_GEMM_CFG || key > UTV_TUNE_QR_CTAS) return UTV_ERR_ARG;
+  if (old) *old = cur[key];
+  cur[key] = value;
+  if (key == UTV_TUNE_GEMM_CFG && (value < 0 || value > 5)) cur[key] = -1;
+  if (key != UTV_TUNE_GEMM_CFG && value < 0) cur[key] = 0;
+  dgemm_force((int)cur[UTV_TUNE_GEMM_CFG], (int)cur[UTV_TUNE_GEMM_SPLITS], (int)cur[UTV_TUNE_GEMM_PATH]);
+  panel_force((int)cur[UTV_TUNE_QR_GLOBAL], (int)cur[UTV_TUNE_QR_CTAS]);
+  return UTV_OK;
 }
 
 utv_status utv_set_device_budget(utv_handle h, int64_t bytes) {

@@ -66,3 +66,33 @@ def test_hbm_kernels_gbs(bench):
     assert out["sketch"]["gbs"] == pytest.approx(6400.0)
     assert out["sketch"]["frac"] == pytest.approx(6400.0 / out["peak_gbs"])
     assert out["peak_gbs"] > 1000.0
+
+
+def test_gpus_n_self_launches_n_ranks():
+    """`python bench.py --gpus 2` with no launcher re-executes itself under torch.distributed.run
+    with 2 ranks (VERDICT r01 missing #2); the gloo dry run checks the rank count, the
+    max-over-ranks timing and the single JSON line of rank 0."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run",
+                        "--steps", "2", "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["ranks_seen"] == 2 and out["dry_run"] is True
+    assert out["steps"] == 2 and out["warmup"] == 3 and out["ms_per_step"] >= 0.0
+
+
+def test_cpu_protocol_fields(bench):
+    """SURVEY 8(d) CPU protocol: CPU model, nproc, 1-core cfg1 time, labelled extrapolation."""
+    pr = bench.cpu_protocol("cfg3", 0.01)
+    assert pr["nproc"] >= 1 and pr["cpu_model"]
+    one = pr["cfg1_one_core"]
+    assert one["cores"] == 1 and one["rank"] == 256 and one["seconds"] > 0
+    ex = pr["extrapolated"]
+    assert "extrapolated" in ex["label"]
+    assert ex["seconds_one_core"] == pytest.approx(ex["f_alg"] / (one["gflops"] * 1e9))
+    assert ex["seconds_all_cores"] == pytest.approx(ex["f_alg"] / 1e10)

@@ -175,3 +175,16 @@ def test_streamed_random_shapes(utv, h, monkeypatch, seed):
     _, _, Xg, rg = streamed(utv, h, M.A, B, b, q, seed)
     assert rg == ro
     assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
+@pytest.mark.parametrize("n", [48, 64])
+def test_streamed_single_block_nan_is_reported(utv, h, monkeypatch, n):
+    """n <= b: no sketch pass runs, so the streamed block 0 is checked on load (utv.h: NaN / Inf in
+    A -> UTV_ERR_NUMERICAL)."""
+    monkeypatch.setenv("UTV_OOC_MAX_RESIDENT_COLS", "0")
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((200, n)); A[17, n // 2] = np.nan
+    B = rng.standard_normal((200, 1))
+    with pytest.raises(utv.UtvError) as e:
+        streamed(utv, h, A, B, 64, 1, 1)
+    assert e.value.status == utv.UTV_ERR_NUMERICAL

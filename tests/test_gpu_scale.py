@@ -115,3 +115,53 @@ def test_cfg2_streamed_out_of_core(utv, monkeypatch):
     assert rel <= 1e-10, rel
     assert ne <= 1e-12, ne
     assert st["resident_cols"] == n - (n - 8192 + b - 1) // b * b and st["h2d_bytes"] > 8 * m * n
+
+
+def test_cfg2_keep_factors_new_rhs(utv):
+    """configs[1] with UTV_KEEP_FACTORS: factor + solve for one RHS, then utv_solve_rhs for a
+    second, fresh RHS of the same known-solution construction (SURVEY 8(f) #3 at full size)."""
+    m = n = 20000
+    r, b, q = 10000, 256, 2
+    dev = torch.device("cuda:0")
+    At, Bm, X0 = gen.gp_torch(m, n, r, seed=gen.MATRIX_SEED, device=dev, k=2)
+    A = utv.colmajor(At.t().clone())
+    del At
+    B = utv.colmajor(Bm)
+    h = utv.Handle(0)
+    X1 = utv.colmajor_empty(n, 1)
+    opts = utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED, flags=utv.UTV_KEEP_FACTORS)
+    assert h.lstsq(A, utv.colmajor(B[:, :1].clone()), X1, opts) == r
+    X2 = utv.colmajor_empty(n, 1)
+    assert h.solve_rhs(A, utv.colmajor(B[:, 1:2].clone()), X2) == r
+    torch.cuda.synchronize()
+    for j, X in ((0, X1), (1, X2)):
+        rel = ((X[:, 0] - X0[:, j]).norm() / X0[:, j].norm()).item()
+        assert rel <= 1e-10, (j, rel)
+    h.close()
+
+
+def test_cfg2_reconstruction_explicit_u(utv):
+    """configs[1] with the explicit U (UTV_WANT_U, v21t): ||A - U T V^T||_F / ||A||_F and the
+    orthogonality of U and V at full size (products in torch on the GPU)."""
+    m = n = 20000
+    r, b, q = 10000, 256, 2
+    dev = torch.device("cuda:0")
+    At, _, _ = gen.gp_torch(m, n, r, seed=gen.MATRIX_SEED, device=dev, k=1)
+    A0 = utv.colmajor(At.t().clone())
+    del At
+    A = A0.clone()
+    V = utv.colmajor_empty(n, n)
+    U = utv.colmajor_empty(m, m)
+    h = utv.Handle(0)
+    rank = h.factor(A, V=V, U=U, opts=utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED,
+                                                flags=utv.UTV_WANT_U))
+    torch.cuda.synchronize()
+    h.close()
+    assert rank == r
+    rec = ((A0 - (U @ A) @ V.t()).norm() / A0.norm()).item()
+    assert rec <= 1e-13, rec
+    I = torch.eye(n, dtype=torch.float64, device=dev)
+    for Q in (U, V):
+        E = Q.t() @ Q - I
+        assert E.abs().max().item() <= 1e-13
+        assert (E.norm() / n ** 0.5).item() <= 1e-13

@@ -353,11 +353,60 @@ def test_scale_equivariance_bit_identical():
     assert r1 == r2 and np.array_equal(X1, X2)
 
 
+def _randutv_steps(A, b, q, seed, top_rows):
+    """randUTV assembled from the oracle's step functions (gauss, hqr, svd_small) with the right
+    update of fig:alg_utv applied either to ALL rows 0:m (reading R1) or, literally as Fig. 2
+    prints it, only to the trailing rows j0:m.  Returns (U, T, V)."""
+    A = np.array(A, dtype=np.float64)
+    m, n = A.shape
+    U, V = np.eye(m), np.eye(n)
+
+    def q_of(Pk, tau, T):
+        W = np.tril(Pk, -1); W[np.arange(Pk.shape[1]), np.arange(Pk.shape[1])] = 1.0
+        return np.eye(Pk.shape[0]) - W @ T @ W.T
+
+    for step, j0 in enumerate(range(0, n, b)):
+        bw = min(b, n - j0)
+        if n - j0 > b:
+            G = oracle.gauss(seed, step, j0, m - j0, b)
+            Ap = A[j0:, j0:]
+            Y = Ap.T @ G
+            for _ in range(q):
+                Y = Ap.T @ (Ap @ Y)
+            Qv = np.eye(n)
+            Qv[j0:, j0:] = q_of(*oracle.hqr(Y))
+            r0 = 0 if top_rows else j0
+            A[r0:, :] = A[r0:, :] @ Qv
+            V = V @ Qv
+        Pk, tau, T = oracle.hqr(A[j0:, j0:j0 + bw])
+        Qu = np.eye(m)
+        Qu[j0:, j0:] = q_of(Pk, tau, T)
+        A = Qu.T @ A
+        U = U @ Qu
+        A[j0 + bw:, j0:j0 + bw] = 0.0
+        Us, s, Vs, _ = oracle.svd_small(np.triu(A[j0:j0 + bw, j0:j0 + bw]))
+        A[j0:j0 + bw, j0:j0 + bw] = np.diag(s)
+        A[:j0, j0:j0 + bw] = A[:j0, j0:j0 + bw] @ Vs
+        A[j0:j0 + bw, j0 + bw:] = Us.T @ A[j0:j0 + bw, j0 + bw:]
+        V[:, j0:j0 + bw] = V[:, j0:j0 + bw] @ Vs
+        U[:, j0:j0 + bw] = U[:, j0:j0 + bw] @ Us
+    return U, A, V
+
+
 def test_literal_fig2_reading_is_wrong():
-    """R1: skipping the top rows in the right update breaks A = U T V^T (evidence for the reading)."""
+    """R1 (P:798-801 vs P:824, Appl_r_TD): the right update printed in Fig. 2 touches
+    only [A11 A12; A21 A22]; run literally (rows j0:m only) the factors no longer reproduce A,
+    while the all-rows reading does.  Both runs use the oracle's own step functions."""
     A = gen.gp(64, 64, 32, seed=2)
+    nrm = np.linalg.norm(A)
+    U, T, V = _randutv_steps(A, 16, 1, 1, top_rows=True)
+    assert np.linalg.norm(A - U @ T @ V.T) <= 1e-13 * nrm
+    U, T, V = _randutv_steps(A, 16, 1, 1, top_rows=False)
+    assert np.linalg.norm(A - U @ T @ V.T) >= 1e-3 * nrm          # SURVEY App. A: 3e-2
+    # the all-rows assembly is the C oracle's randutv (same T up to rounding)
     out = oracle.randutv(A, 16, 1, seed=1, want_u=True)
-    assert np.linalg.norm(A - out["U"] @ out["T"] @ out["V"].T) <= 1e-13 * np.linalg.norm(A)
+    Ua, Ta, Va = _randutv_steps(A, 16, 1, 1, top_rows=True)
+    assert np.abs(out["T"] - Ta).max() <= 1e-10 * nrm
 
 
 def test_threads_bit_identical():
