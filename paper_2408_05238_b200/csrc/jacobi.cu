@@ -148,6 +148,7 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
                   jj[row] = sn * u[k] + cs * v[k];
                 }
               }
+              __syncwarp();                                  // every lane has read s_nrm[a], s_nrm[b]
               if (lane == 0) {
                 s_nrm[a] = fmax(al - t * gm, 0.0);
                 s_nrm[b] = be + t * gm;
