@@ -77,13 +77,20 @@ utv_status utv_rank_diag(utv_handle handle, int64_t n, const double* d, double t
  *   UTV_TUNE_GEMM_PATH    1 = the cp.async kernel instead of the TMA kernel (0 = automatic)
  *   UTV_TUNE_QR_GLOBAL    1 = the global-memory sub-panel kernel of a3/a5 at any panel height
  *   UTV_TUNE_QR_CTAS      cap on the cooperative CTAs of a sub-panel launch (0 = automatic)
+ *   UTV_TUNE_DIST_CHUNKS  multi-GPU handles: column chunks (1..4) of the sketch / power-iteration
+ *                         and X = A W_V products, each chunk's AllReduce overlapping the next
+ *                         chunk's GEMM on the communication stream (0 = automatic: 2)
+ *   UTV_TUNE_SVD_LAG      multi-GPU handles: steps (1..8) by which the application of a diagonal
+ *                         block's SVD may trail its panel QR (0 = automatic: 1 at P = 1, else 8)
  * Returns UTV_ERR_ARG for an unknown key; *old (if non-NULL) gets the previous value. */
 enum {
   UTV_TUNE_GEMM_CFG = 1,
   UTV_TUNE_GEMM_SPLITS = 2,
   UTV_TUNE_GEMM_PATH = 3,
   UTV_TUNE_QR_GLOBAL = 4,
-  UTV_TUNE_QR_CTAS = 5
+  UTV_TUNE_QR_CTAS = 5,
+  UTV_TUNE_DIST_CHUNKS = 6,
+  UTV_TUNE_SVD_LAG = 7
 };
 utv_status utv_tune(int key, int64_t value, int64_t* old);
 

@@ -112,6 +112,24 @@ __device__ __forceinline__ void grid_sync_all(unsigned* bar, unsigned nblocks, u
   gen = next;
   __syncthreads();
 }
+// grid_sync_all split in two so that a CTA can do independent work between publishing its arrival
+// and polling for the others' (the qr2 kernel assembles the previous dlarft column of T there).
+__device__ __forceinline__ void grid_arrive(unsigned* bar, unsigned gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu(bar + 32 + blockIdx.x * kFlagStride, gen + 1);
+  }
+}
+__device__ __forceinline__ void grid_wait(unsigned* bar, unsigned nblocks, unsigned& gen) {
+  const unsigned next = gen + 1;
+  for (unsigned c = threadIdx.x; c < nblocks; c += blockDim.x) {
+    while ((int)(ld_relaxed_gpu(bar + 32 + c * kFlagStride) - next) < 0) { }
+    (void)ld_acquire_gpu(bar + 32 + c * kFlagStride);
+  }
+  gen = next;
+  __syncthreads();
+}
 __device__ __forceinline__ void grid_sync_finish(unsigned* bar, unsigned gen) {
   if (blockIdx.x == 0 && threadIdx.x == 0) st_release_gpu(bar, gen);
 }

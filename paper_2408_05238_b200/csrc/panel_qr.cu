@@ -138,6 +138,20 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     (void)j; (void)ph;
 #endif
   };
+  // dlarft column j of T (T[0:j, j] = -tau_j T[0:j, 0:j] s_j, T[j, j] = tau_j; s_j = ssg) is
+  // assembled by CTA 0 one column LATE, between publishing its arrival at column j+1's grid barrier
+  // and polling for the others -- off the per-column critical path (thread l < j owns row l of T;
+  // ssg keeps column j's values until column j+1's dlarfg, after the barrier).
+  double tj_prev = 0.0;
+  auto t_column = [&](int jc, double tjc) {
+    if (blockIdx.x != 0 || jc < 0) return;
+    if (tid < jc) {
+      double s = 0.0;
+      for (int l = tid; l < jc; ++l) s += sT[tid * NBMAX + l] * ssg[l];
+      sT[tid * NBMAX + jc] = -tjc * s;
+    }
+    if (tid == 0) { sT[jc * NBMAX + jc] = tjc; tau[jc] = tjc; }
+  };
   for (int j = 0; j < nb; ++j) {
     tr(j, 0);
     const int buf = j & 1;
@@ -145,6 +159,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     if (G == 1) {
       block_reduce_store<false>(acc, nb, red_w, red, 1);
       if (tid < nb) piv[tid] = SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)];
+      t_column(j - 1, tj_prev);
       __syncthreads();
     } else {
       block_reduce_store<true>(acc, nb, red_w, pelem(buf, 0, blockIdx.x), (int)G);
@@ -154,7 +169,9 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
 #ifdef UTV_QR_TRACE
       if (j == 5 && tid == 0 && blockIdx.x < 256) g_qr_arrive[blockIdx.x] = gtimer();
 #endif
-      grid_sync_all(bar, G, gen);
+      grid_arrive(bar, gen);
+      t_column(j - 1, tj_prev);
+      grid_wait(bar, G, gen);
 #ifdef UTV_QR_TRACE
       if (j == 5 && tid == 0 && blockIdx.x < 256) g_qr_arrive[256 + blockIdx.x] = gtimer();
 #endif
@@ -207,15 +224,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     }
     if (SMEM && tid < NBMAX) swz[tid] = (tid > j && tid < nb) ? piv[tid] + red[tid] * scal : 0.0;
     __syncthreads();
-    if (blockIdx.x == 0) {
-      // dlarft: T[0:j, j] = -tau_j T[0:j, 0:j] s ; T[j, j] = tau_j
-      if (tid < j) {
-        double s = 0.0;
-        for (int l = tid; l < j; ++l) s += sT[tid * NBMAX + l] * ssg[l];
-        sT[tid * NBMAX + j] = -tj * s;
-      }
-      if (tid == 0) { sT[j * NBMAX + j] = tj; tau[j] = tj; }
-    }
+    tj_prev = tj;
 #pragma unroll
     for (int v = 0; v < NBMAX; ++v) acc[v] = 0.0;
     tr(j, 2);
@@ -291,6 +300,8 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     }
     __syncthreads();
   }
+  t_column(nb - 1, tj_prev);                 // the last column of T
+  __syncthreads();
   // write back: P = R (upper) / 0 (below); W = explicit unit-lower Householder vectors
   for (int64_t e = tid; e < (r1 - r0) * nb; e += QR_THREADS) {
     const int64_t il = e % (r1 - r0), c = e / (r1 - r0), i = r0 + il;

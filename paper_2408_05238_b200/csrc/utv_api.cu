@@ -280,6 +280,12 @@ struct utv_handle_s {
   unsigned* bar2 = nullptr;      // grid-barrier state of the SVD side stream
   cudaStream_t side = nullptr;   // a7 (small SVD + its 4 updates) overlaps the next step's sketch
   cudaEvent_t ev_panel = nullptr, ev_svd = nullptr, ev_us = nullptr;
+  // multi-GPU overlap: collectives of column chunks run on a communication stream (high priority)
+  // while the main stream computes the next chunk; the owner's SVDs may lag up to kLagMax steps
+  static constexpr int kChunks = 4, kLagMax = 8;
+  cudaStream_t cst = nullptr;
+  cudaEvent_t ev_cq[kChunks] = {}, ev_cd[kChunks] = {};
+  cudaEvent_t ev_svdq[kLagMax + 1] = {};
   int* info = nullptr;           // Jacobi sweeps / failure flag
   int* flag = nullptr;           // finiteness flag
   int64_t* d_rank = nullptr;
@@ -308,6 +314,9 @@ struct utv_handle_s {
 };
 
 namespace {
+
+int g_dist_chunks = 0;   // utv_tune(UTV_TUNE_DIST_CHUNKS): 0 = automatic
+int g_svd_lag = 0;       // utv_tune(UTV_TUNE_SVD_LAG): 0 = automatic
 
 struct ApiError {
   utv_status st;
@@ -1273,7 +1282,8 @@ int64_t dist_local_cols(int64_t n, int64_t b, int P, int p) {
 
 size_t dist_dbuf_doubles(int64_t n, int64_t b, int P, int64_t k) {
   const int64_t nb = (n + b - 1) / b, Lmax = (nb + P - 1) / P * b;
-  return (size_t)Lmax * b * (P + 1) + n + 64 + 2 * (size_t)b * (size_t)std::max<int64_t>(k, 1) + 64;
+  return (size_t)Lmax * b * (P + 1) + n + 64 + 2 * (size_t)b * (size_t)std::max<int64_t>(k, 1) + 64 +
+         (size_t)(utv_handle_s::kLagMax + 1) * (size_t)(b * b + b);
 }
 
 // Every device allocation lstsq_dist makes, done up front (before the ranks agree on the call).
@@ -1346,7 +1356,7 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   const int P = comm.nranks, p = comm.rank;
   const int64_t b = opt.block, nb = (n + b - 1) / b;
   const int64_t nloc = dist_local_cols(n, b, P, p);
-  cudaStream_t st = h->stream;
+  cudaStream_t st = h->stream, cs = h->cst;
   const int ns = h->num_sms;
   Ctx c = make_ctx(h, m, n, k, b);
   const Layout& L = c.L;
@@ -1369,39 +1379,71 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   double* sbuf = dg + n + 64;
   double* zb = sbuf + (size_t)b * kk;
   double* flags = zb + (size_t)b * kk;
+  double* usring = flags + 64;                                   // (kLagMax+1) x b^2: pending U_s
+  double* sgring = usring + (size_t)(utv_handle_s::kLagMax + 1) * b * b;   // (kLagMax+1) x b: sigma
   UTV_CUDA(cudaMemsetAsync(h->info, 0, 4 * sizeof(int), st));
   UTV_CUDA(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
   if (nloc > 0) launch_check_finite(st, m, nloc, A, lda, h->flag);
   if (k > 0) launch_check_finite(st, m, k, B, ldb, h->flag);
   double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *WP = c.at(L.Wv), *Xa = c.at(L.X), *LU = c.at(L.Wu);
   double *Tu = c.at(L.Tu), *tauu = c.at(L.tauu), *tauv = c.at(L.tauv), *S = c.at(L.S), *Z1 = c.at(L.Z1);
-  double *Z2 = c.at(L.Z2), *tmp = c.at(L.tmp2), *Us = c.at(L.Us), *sig = c.at(L.sig), *Yl = c.at(L.tmp);
+  double *Z2 = c.at(L.Z2), *Yl = c.at(L.tmp);
 
-  bool pend = false, us_applied = false;             // deferred SVD application (see a7 below)
-  int64_t p_i = 0, p_j0 = 0, p_bw = 0, p_lr = 0, p_nrl = 0;
-  int p_owner = 0;
-  auto apply_pending = [&]() {
-    if (!pend) return;
-    if (p == p_owner) UTV_CUDA(cudaStreamWaitEvent(st, h->ev_svd, 0));
-    double* Usp = kp ? kp->Us + (size_t)p_i * b * b : ((p_i & 1) ? c.at(L.Us2) : Us);
-    double* sgp = (p_i & 1) ? c.at(L.sig2) : sig;
-    double* Vsp = fv.Vs + (size_t)p_i * b * b;
-    comm.bcast(Usp, (size_t)b * b, p_owner, st);
-    comm.bcast(Vsp, (size_t)b * b, p_owner, st);
-    comm.bcast(sgp, (size_t)b, p_owner, st);
-    launch_copy(st, p_bw, 1, sgp, p_bw, dg + p_j0, n);
-    if (p_nrl > 0) {                                                                    // A12 := U_s^T A12
-      double* A12 = A + cm(p_j0, p_lr, lda);
-      c.gemm(true, false, p_bw, p_nrl, p_bw, 1.0, Usp, b, A12, lda, 0.0, Yl, p_bw);
-      launch_copy(st, p_bw, p_nrl, Yl, p_bw, A12, lda);
+  // Column chunks of the b sketch columns: the power iteration is column-separable
+  // (Y = (A'^T A')^q A'^T G, one column of G at a time), and so is X = A W_V, so chunk c's
+  // AllReduce (communication stream) overlaps chunk c+1's GEMM (main stream).  SURVEY 8(e) overlap.
+  const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(g_dist_chunks > 0 ? g_dist_chunks : (P > 1 ? 2 : 1), b));
+  auto chunk = [&](int q, int64_t* c0, int64_t* c1) {
+    *c0 = b * q / nch; *c1 = b * (q + 1) / nch;
+  };
+  // comm stream joins the main stream's history once (buffers it reduces were written there)
+  UTV_CUDA(cudaEventRecord(h->ev_panel, st));
+  UTV_CUDA(cudaStreamWaitEvent(cs, h->ev_panel, 0));
+  // produce(q) enqueues chunk q's product on the main stream; its AllReduce goes to the comm
+  // stream; join() makes the main stream wait for every chunk's reduction.
+  auto reduce_chunk = [&](int q, double* buf, size_t cnt) {
+    UTV_CUDA(cudaEventRecord(h->ev_cq[q], st));
+    UTV_CUDA(cudaStreamWaitEvent(cs, h->ev_cq[q], 0));
+    comm.allreduce(buf, cnt, cs);
+    UTV_CUDA(cudaEventRecord(h->ev_cd[q], cs));
+  };
+  auto wait_chunk = [&](int q) { UTV_CUDA(cudaStreamWaitEvent(st, h->ev_cd[q], 0)); };
+
+  // a7 of block i runs on its owner's side stream right after block i's panel QR; everything it
+  // changes in A (A11 := Sigma excepted), C and diag(T) is applied on the main stream `lag` steps
+  // later, in block order, on every rank (broadcast from the owner).  Reading H5: U_s^T acts on
+  // rows of block i that later steps only right-multiply (A12, and the top-row updates), and A01 V_s
+  // on columns no later step reads, so left and right factors commute; applying them on the main
+  // stream in block order keeps every read-modify-write of those rows / columns ordered.
+  const int lag = (int)std::max<int64_t>(1, g_svd_lag > 0 ? g_svd_lag : (P > 1 ? utv_handle_s::kLagMax : 1));
+  struct Pend { int64_t i, j0, bw, lt, lr, nrl; int owner; };
+  std::vector<Pend> pend;                          // FIFO (front = oldest)
+  size_t pend_head = 0;
+  auto apply_front = [&]() {
+    const Pend e = pend[pend_head++];
+    const int slot = (int)(e.i % (utv_handle_s::kLagMax + 1));
+    double* Usp = kp ? kp->Us + (size_t)e.i * b * b : usring + (size_t)slot * b * b;
+    double* sgp = sgring + (size_t)slot * b;
+    double* Vsp = fv.Vs + (size_t)e.i * b * b;
+    if (p == e.owner) UTV_CUDA(cudaStreamWaitEvent(st, h->ev_svdq[slot], 0));
+    comm.bcast(Usp, (size_t)b * b, e.owner, st);
+    comm.bcast(Vsp, (size_t)b * b, e.owner, st);
+    comm.bcast(sgp, (size_t)b, e.owner, st);
+    launch_copy(st, e.bw, 1, sgp, e.bw, dg + e.j0, n);
+    if (p == e.owner && e.j0 > 0) {                                                    // A01 := A01 V_s
+      double* A01 = A + cm(0, e.lt, lda);
+      c.gemm(false, false, e.j0, e.bw, e.bw, 1.0, A01, lda, Vsp, b, 0.0, Yl, e.j0);
+      launch_copy(st, e.j0, e.bw, Yl, e.j0, A01, lda);
+    }
+    if (e.nrl > 0) {                                                                    // A12 := U_s^T A12
+      double* A12 = A + cm(e.j0, e.lr, lda);
+      c.gemm(true, false, e.bw, e.nrl, e.bw, 1.0, Usp, b, A12, lda, 0.0, Yl, e.bw);
+      launch_copy(st, e.bw, e.nrl, Yl, e.bw, A12, lda);
     }
     if (k > 0) {                                                                        // C1 := U_s^T C1
-      c.gemm(true, false, p_bw, k, p_bw, 1.0, Usp, b, B + p_j0, ldb, 0.0, Z1, p_bw);
-      launch_copy(st, p_bw, k, Z1, p_bw, B + p_j0, ldb);
+      c.gemm(true, false, e.bw, k, e.bw, 1.0, Usp, b, B + e.j0, ldb, 0.0, Z1, e.bw);
+      launch_copy(st, e.bw, k, Z1, e.bw, B + e.j0, ldb);
     }
-    UTV_CUDA(cudaEventRecord(h->ev_us, st));
-    us_applied = true;
-    pend = false;
   };
   for (int64_t i = 0, j0 = 0; i < nb; ++i, j0 += b) {
     const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0;
@@ -1420,10 +1462,19 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
       launch_sketch(st, opt.seed, i, j0, mp, b, G, mp, ns);                           // a1
       if (ncl) c.gemm(true, false, ncl, b, mp, 1.0, At, lda, G, mp, 0.0, Yl, ldwp);
       for (int32_t it = 0; it < opt.power_iters; ++it) {                              // a2 (R7)
-        if (ncl) c.gemm(false, false, mp, b, ncl, 1.0, At, lda, Yl, ldwp, 0.0, Z, mp);
-        else launch_set_zero(st, mp, b, Z, mp);
-        comm.allreduce(Z, (size_t)mp * b, st);
-        if (ncl) c.gemm(true, false, ncl, b, mp, 1.0, At, lda, Z, mp, 0.0, Yl, ldwp);
+        for (int q = 0; q < nch; ++q) {                                               // Z_q = A' Y_q
+          int64_t c0, c1; chunk(q, &c0, &c1);
+          double* Zq = Z + (size_t)mp * c0;
+          if (ncl) c.gemm(false, false, mp, c1 - c0, ncl, 1.0, At, lda, Yl + c0 * ldwp, ldwp, 0.0, Zq, mp);
+          else launch_set_zero(st, mp, c1 - c0, Zq, mp);
+          reduce_chunk(q, Zq, (size_t)mp * (c1 - c0));                                // AllReduce(Z_q)
+        }
+        for (int q = 0; q < nch; ++q) {                                               // Y_q = A'^T Z_q
+          int64_t c0, c1; chunk(q, &c0, &c1);
+          wait_chunk(q);
+          if (ncl) c.gemm(true, false, ncl, c1 - c0, mp, 1.0, At, lda, Z + (size_t)mp * c0, mp, 0.0, Yl + c0 * ldwp,
+                          ldwp);
+        }
       }
       launch_copy(st, ncl, b, Yl, ldwp, Ypad, Lmax);                                  // AllGather(Y)
       comm.allgather(Ypad, recv, (size_t)Lmax * b, st);
@@ -1433,15 +1484,25 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
       double* Wv = fv.W + fv.woff.back();
       panel_qr(st, np, b, Y, np, Wv, np, tauv, Tvs, b, c.pw);                          // a3 (same on all)
       launch_gather_local(st, ncl, b, b, i, P, p, Wv, np, WP, ldwp);                   // my rows of W_V
-      if (ncl) c.gemm(false, false, m, b, ncl, 1.0, A + cm(0, lt, lda), lda, WP, ldwp, 0.0, Xa, m);
-      else launch_set_zero(st, m, b, Xa, m);
-      comm.allreduce(Xa, (size_t)m * b, st);                                          // a4, R1
+      for (int q = 0; q < nch; ++q) {                                                 // X_q = A W_V,q
+        int64_t c0, c1; chunk(q, &c0, &c1);
+        double* Xq = Xa + (size_t)m * c0;
+        if (ncl) c.gemm(false, false, m, c1 - c0, ncl, 1.0, A + cm(0, lt, lda), lda, WP + c0 * ldwp, ldwp, 0.0, Xq, m);
+        else launch_set_zero(st, m, c1 - c0, Xq, m);
+        reduce_chunk(q, Xq, (size_t)m * (c1 - c0));                                   // a4, R1: AllReduce
+      }
+      for (int q = 0; q < nch; ++q) wait_chunk(q);
       c.gemm(false, false, m, b, b, 1.0, Xa, m, Tvs, b, 0.0, X2, m);
       if (j0 > 0 && ncl) c.gemm(false, true, j0, ncl, b, -1.0, X2, m, WP, ldwp, 1.0, A + cm(0, lt, lda), lda);
       if (own) c.gemm(false, true, mp, bw, b, -1.0, X2 + j0, m, WP, ldwp, 1.0, At, lda);
     }
-    if (own) panel_qr(st, mp, bw, At, lda, Wu, m, tauu, Tu, b, c.pw);                   // a5
-    comm.bcast(LU + cm(0, b, m), (size_t)m * b, owner, st);
+    // a5 on the owner; Broadcast(W_U) of the live rows j0:m only, packed (Xa is free here)
+    if (own) {
+      panel_qr(st, mp, bw, At, lda, Wu, m, tauu, Tu, b, c.pw);
+      launch_copy(st, mp, bw, Wu, m, Xa, mp);
+    }
+    comm.bcast(Xa, (size_t)mp * bw, owner, st);
+    if (!own) launch_copy(st, mp, bw, Xa, mp, Wu, m);
     comm.bcast(Tu, (size_t)b * b, owner, st);
     if (kp) kept_push_u(st, *kp, i, mp, bw, Wu, m, Tu);                                  // keep W_U, T_U
     if (nrl > 0) {                                                                      // a6, R3
@@ -1464,31 +1525,26 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
       c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
       c.gemm(false, false, mp, k, bw, -1.0, Wu, m, Z2, bw, 1.0, Cr, ldb);
     }
-    // a7: the SVD of step i runs on the owner's side stream; its results are broadcast and applied
-    // at the end of step i+1 (same point in every rank's sequence of collectives), so no rank waits
-    // for the Jacobi: A12 := U_s^T A12 commutes with the intervening right updates (as on one GPU),
-    // V_s and sigma are only needed by the solve, U_s^T C1 touches rows no later step reads.
-    apply_pending();
+    // a7: the owner's side stream computes (U_s, sigma, V_s) of R = A11 and writes A11 := Sigma
+    // (nothing on the main stream touches A11 after the panel QR); the rest is applied `lag` steps
+    // later (apply_front), at the same point of every rank's sequence of collectives.
     if (own) {
+      const int slot = (int)(i % (utv_handle_s::kLagMax + 1));
       double* Vsi = fv.Vs + (size_t)i * b * b;
-      double* Usi = kp ? kp->Us + (size_t)i * b * b : ((i & 1) ? c.at(L.Us2) : Us);
-      double* sgi = (i & 1) ? c.at(L.sig2) : sig;
+      double* Usi = kp ? kp->Us + (size_t)i * b * b : usring + (size_t)slot * b * b;
+      double* sgi = sgring + (size_t)slot * b;
       UTV_CUDA(cudaEventRecord(h->ev_panel, st));
       UTV_CUDA(cudaStreamWaitEvent(c.side, h->ev_panel, 0));
       svd_small(c.side, bw, At, lda, Usi, b, sgi, Vsi, b, c.sw);
       launch_set_diag(c.side, bw, sgi, At, lda);
-      if (j0 > 0) {                                                                     // A01 := A01 V_s
-        if (us_applied) UTV_CUDA(cudaStreamWaitEvent(c.side, h->ev_us, 0));         // its rows j0-b:j0
-        c.gemm_side(false, false, j0, bw, bw, 1.0, A + cm(0, lt, lda), lda, Vsi, b, 0.0, tmp, j0);
-        launch_copy(c.side, j0, bw, tmp, j0, A + cm(0, lt, lda), lda);
-      }
-      UTV_CUDA(cudaEventRecord(h->ev_svd, c.side));
+      UTV_CUDA(cudaEventRecord(h->ev_svdq[slot], c.side));
     }
-    pend = true;
-    p_i = i; p_j0 = j0; p_bw = bw; p_owner = owner; p_lr = lr; p_nrl = nrl;
+    pend.push_back(Pend{i, j0, bw, lt, lr, nrl, owner});
+    while (pend.size() - pend_head > (size_t)lag) apply_front();
   }
-  apply_pending();
-  // every rank fails alike: AllReduce the local NaN / Jacobi flags
+  while (pend_head < pend.size()) apply_front();
+  // every rank fails alike: AllReduce the local NaN / Jacobi flags (the owners' side-stream SVDs
+  // were all joined by apply_front)
   UTV_CUDA(cudaMemcpyAsync(h->h_info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   UTV_CUDA(cudaMemcpyAsync(h->h_info + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   comm.wait(st);
@@ -1545,6 +1601,13 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_panel, cudaEventDisableTiming));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_svd, cudaEventDisableTiming));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_us, cudaEventDisableTiming));
+    UTV_CUDA(cudaStreamCreateWithPriority(&h->cst, cudaStreamNonBlocking, hi));
+    for (int q = 0; q < utv_handle_s::kChunks; ++q) {
+      UTV_CUDA(cudaEventCreateWithFlags(&h->ev_cq[q], cudaEventDisableTiming));
+      UTV_CUDA(cudaEventCreateWithFlags(&h->ev_cd[q], cudaEventDisableTiming));
+    }
+    for (int q = 0; q <= utv_handle_s::kLagMax; ++q)
+      UTV_CUDA(cudaEventCreateWithFlags(&h->ev_svdq[q], cudaEventDisableTiming));
     UTV_CUDA(cudaMalloc((void**)&h->info, 64 * sizeof(int)));
     UTV_CUDA(cudaMalloc((void**)&h->flag, sizeof(int)));
     UTV_CUDA(cudaMalloc((void**)&h->agree, 2 * sizeof(double)));
@@ -1630,9 +1693,16 @@ utv_status utv_destroy(utv_handle h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream); else cudaDeviceSynchronize();
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
+  if (h->cst) { cudaStreamSynchronize(h->cst); cudaStreamDestroy(h->cst); }
   if (h->ev_panel) cudaEventDestroy(h->ev_panel);
   if (h->ev_svd) cudaEventDestroy(h->ev_svd);
   if (h->ev_us) cudaEventDestroy(h->ev_us);
+  for (int q = 0; q < utv_handle_s::kChunks; ++q) {
+    if (h->ev_cq[q]) cudaEventDestroy(h->ev_cq[q]);
+    if (h->ev_cd[q]) cudaEventDestroy(h->ev_cd[q]);
+  }
+  for (int q = 0; q <= utv_handle_s::kLagMax; ++q)
+    if (h->ev_svdq[q]) cudaEventDestroy(h->ev_svdq[q]);
   if (h->h2d) { cudaStreamSynchronize(h->h2d); cudaStreamDestroy(h->h2d); }
   if (h->d2h) { cudaStreamSynchronize(h->d2h); cudaStreamDestroy(h->d2h); }
   for (int s = 0; s < utv_handle_s::kStg; ++s) {
@@ -2042,15 +2112,17 @@ utv_status utv_rank(utv_handle h, int64_t n, const double* T, int64_t ldt, doubl
 
 utv_status utv_tune(int key, int64_t value, int64_t* old) {
   static std::mutex mu;
-  static int64_t cur[6] = {0, -1, 0, 0, 0, 0};
+  static int64_t cur[8] = {0, -1, 0, 0, 0, 0, 0, 0};
   std::lock_guard<std::mutex> lk(mu);
-  if (key < UTV_TUNE_GEMM_CFG || key > UTV_TUNE_QR_CTAS) return UTV_ERR_ARG;
+  if (key < UTV_TUNE_GEMM_CFG || key > UTV_TUNE_SVD_LAG) return UTV_ERR_ARG;
   if (old) *old = cur[key];
   cur[key] = value;
   if (key == UTV_TUNE_GEMM_CFG && (value < 0 || value > 5)) cur[key] = -1;
   if (key != UTV_TUNE_GEMM_CFG && value < 0) cur[key] = 0;
   dgemm_force((int)cur[UTV_TUNE_GEMM_CFG], (int)cur[UTV_TUNE_GEMM_SPLITS], (int)cur[UTV_TUNE_GEMM_PATH]);
   panel_force((int)cur[UTV_TUNE_QR_GLOBAL], (int)cur[UTV_TUNE_QR_CTAS]);
+  g_dist_chunks = (int)std::min<int64_t>(cur[UTV_TUNE_DIST_CHUNKS], utv_handle_s::kChunks);
+  g_svd_lag = (int)std::min<int64_t>(cur[UTV_TUNE_SVD_LAG], utv_handle_s::kLagMax);
   return UTV_OK;
 }
 

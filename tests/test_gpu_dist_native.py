@@ -221,3 +221,31 @@ def test_local_group_nan_on_one_rank_fails_all(utv):
     finally:
         for h in hs:
             h.close()
+
+
+@pytest.mark.parametrize("P,chunks,lag", [(2, 1, 1), (2, 3, 5), (3, 4, 8), (3, 2, 2), (1, 2, 8)])
+def test_local_group_chunks_and_svd_lag(utv, P, chunks, lag):
+    """The overlap schedule of the multi-GPU path: the power-iteration and X = A W_V
+    products in `chunks` column chunks (each chunk's AllReduce on the communication stream) and
+    the SVD of a diagonal block applied `lag` steps after its panel QR.  Against the oracle (x to
+    1e-9, r identical).  A later U_s^T / V_s only reorders commuting factors (reading H5), so X
+    agrees with lag 1 to rounding."""
+    m, n, r, b, q, k = 700, 650, 300, 64, 2, 2
+    M = gen.GpMatrix(m, n, r, seed=31 + P)
+    B, X0 = M.known_rhs(k=k)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=5)
+    res = {}
+    for lg in sorted({1, lag}):
+        hs = utv.local_group(P)
+        try:
+            with utv.tuned(utv.UTV_TUNE_DIST_CHUNKS, chunks), utv.tuned(utv.UTV_TUNE_SVD_LAG, lg):
+                Xs, rs = run_group(utv, hs, M.A, B, b, q, 5)
+        finally:
+            for h in hs:
+                h.close()
+        assert all(x == ro == r for x in rs), (rs, ro)
+        for X in Xs:
+            assert np.array_equal(X, Xs[0])
+        assert np.linalg.norm(Xs[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)
+        res[lg] = Xs[0]
+    assert np.linalg.norm(res[1] - res[lag]) <= 1e-12 * np.linalg.norm(res[1])
