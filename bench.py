@@ -129,9 +129,9 @@ def big_gemm_stats(path):
 
 def gemm_traffic():
     """DRAM traffic per launch of the dominant GEMM launch of the step (cfg3 step-0 sketch product),
-    from the committed ncu --set full capture (profiles/r01_gemm_traffic.json)."""
+    from the committed ncu --set full capture (profiles/r02_gemm_traffic.json)."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")))
         l0 = d["launches"][0]
         return {"traffic": l0["traffic_bytes"], "traffic_algorithmic": l0["algorithmic_bytes"],
                 "traffic_launch": l0["shape"] + "; " + d["source"]}
