@@ -584,10 +584,97 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_streamed_dist(args):
+    """Out-of-core x multi-GPU (UTV_HOST_STREAMED on a utv_create_dist handle; SURVEY 8(e) with
+    8(f) #1, the north star's cfg5 regime): every rank keeps its block-cyclic shard of A in its own
+    pinned host memory, at most --streamed of its columns resident in HBM; B, X on the device."""
+    import torch
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device(f"cuda:{torch.cuda.current_device()}")
+    import paper_2408_05238_b200 as utv
+    import utv_inputs as gen
+    from paper_2408_05238_b200 import dist as D
+    m, n, r_true, b, q, k = CONFIGS[args.config]
+    opts = utv.Opts(block=b, power_iters=q, tau=1e-10, seed=gen.SKETCH_SEED, flags=utv.UTV_HOST_STREAMED)
+    os.environ["UTV_OOC_MAX_RESIDENT_COLS"] = str(args.streamed)
+    At, Bm, X0 = gen.gp_torch(m, n, r_true, seed=gen.MATRIX_SEED, device=dev, k=k)
+    S0 = D.scatter_columns(At.t(), b, world, rank)
+    nloc = S0.shape[1]
+    A0 = utv.colmajor_empty(m, max(nloc, 1), device="cpu", pin_memory=True)
+    A0[:, :nloc].copy_(S0)
+    B0 = utv.colmajor(Bm)
+    del At, S0
+    torch.cuda.empty_cache()
+    uid = [utv.get_unique_id() if rank == 0 else None]
+    if world > 1:
+        torch.distributed.broadcast_object_list(uid, src=0)
+    h = utv.dist_handle(uid[0], world, rank, device=dev.index)
+    Ah = utv.colmajor_empty(m, max(nloc, 1), device="cpu", pin_memory=True)
+    B = utv.colmajor_empty(m, k, device=dev)
+    X = utv.colmajor_empty(n, k, device=dev)
+    times, r = [], -1
+    clocks = ClockSampler(dev.index)
+    for it in range(args.warmup + args.steps):
+        Ah.copy_(A0)
+        B.copy_(B0)
+        if it == args.warmup:
+            clocks.start()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(h.stream)
+        r = h.lstsq(Ah, B, X, opts)
+        e1.record(h.stream)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    clk = clocks.stop()
+    st = h.stream_stats()
+    t = max_over_ranks(statistics.median(times), world, dev)
+    h2d = max_over_ranks(float(st["h2d_bytes"]), world, dev)
+    d2h = max_over_ranks(float(st["d2h_bytes"]), world, dev)
+    rel = float(((X - X0).norm() / X0.norm()).item())
+    F = f_alg(m, n, b, q, k, r)
+    F_exec = F - v_accum_flops(m, n, b) + factored_apply_flops(n, b, k, r)
+    peaks = json.load(open(FP64_PEAK_FILE))
+    t_link = max(h2d / (peaks["h2d_pinned_gbs"] * 1e9), d2h / (peaks["d2h_pinned_gbs"] * 1e9))
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": F_exec / t / 1e12, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "time_to_solution_s": t, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "ours-streamed-dist",
+            "config": {"workload": f"{args.config} out-of-core x multi-GPU (UTV_HOST_STREAMED on a "
+                                   f"utv_create_dist handle): each rank's shard in pinned host memory, <= "
+                                   f"{args.streamed} of its columns resident", "m": m, "n": n, "rank": r_true,
+                       "block": b, "power_iters": q, "rhs": k, "parallelism": f"blockcyclic{world}",
+                       "step": "copy the shard into pinned host memory and B to the device (untimed) + utv_lstsq"},
+            "rank": r, "rank_ok": r == r_true, "rel_err_x0": rel,
+            "stream_max_rank": {"h2d_bytes": h2d, "d2h_bytes": d2h, "resident_cols": st["resident_cols"]},
+            "roofline": {"kernel": "host<->device column-chunk streaming of each rank's shard", "bound": "host-link",
+                         "achieved": h2d / t / 1e9, "peak": peaks["h2d_pinned_gbs"], "unit": "GB/s",
+                         "frac": t_link / t, "traffic": h2d + d2h,
+                         "peak_source": "profiles/r01_fp64_peaks.json: pinned H2D / D2H copy bandwidth"},
+            "clocks": clk}), flush=True)
+    h.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_streamed(args):
     """Out-of-core mode (UTV_HOST_STREAMED): A in pinned host memory, at most
     --streamed columns resident in HBM, the rest streamed every pass.  Bound: the host link."""
     import torch
+    world, _, _ = dist_setup(args)
+    if world > 1 or args.force_dist:
+        return run_streamed_dist(args)
     torch.cuda.set_device(0)
     dev = torch.device("cuda:0")
     import paper_2408_05238_b200 as utv

@@ -114,12 +114,13 @@ __device__ __forceinline__ void grid_sync_all(unsigned* bar, unsigned nblocks, u
 }
 // grid_sync_all split in two so that a CTA can do independent work between publishing its arrival
 // and polling for the others' (the qr2 kernel assembles the previous dlarft column of T there).
+// The arrival is ONE release store: bar.sync orders the CTA's earlier writes (the partial sums,
+// the pivot row) before thread 0's st.release.gpu (PTX memory model: causality order is
+// transitive through the CTA-scope barrier and the GPU-scope release/acquire pair), so no
+// separate __threadfence (MEMBAR.SC.GPU + L1 invalidate in SASS) precedes it.
 __device__ __forceinline__ void grid_arrive(unsigned* bar, unsigned gen) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release_gpu(bar + 32 + blockIdx.x * kFlagStride, gen + 1);
-  }
+  if (threadIdx.x == 0) st_release_gpu(bar + 32 + blockIdx.x * kFlagStride, gen + 1);
 }
 __device__ __forceinline__ void grid_wait(unsigned* bar, unsigned nblocks, unsigned& gen) {
   const unsigned next = gen + 1;

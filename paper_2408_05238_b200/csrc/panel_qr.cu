@@ -75,12 +75,14 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NBMAX], int nb,
 // zeros below R written at the end.  CTA c owns rows [c L, (c+1) L); SMEM: those rows live in
 // shared memory for the whole kernel, else each row is re-read from global (L2) per column with
 // all its loads in flight.  One grid barrier per column.
-template <bool SMEM>
+template <bool SMEM, bool HYB = false>
 __global__ void __launch_bounds__(QR_THREADS, 1)
 qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __restrict__ W, int64_t ldw, int64_t wtop,
            double* __restrict__ tau, double* __restrict__ T, int64_t ldt, double* __restrict__ part,
-           unsigned* __restrict__ bar) {
-  extern __shared__ double sp[];             // [L][SROW] (SMEM only)
+           unsigned* __restrict__ bar, int64_t Ls) {
+  // SMEM: the first Ls rows of each CTA's range live in shared memory for the whole kernel, the
+  // rest (tall panels: hybrid) are re-read from global memory / L2 per column; !SMEM: Ls = 0.
+  extern __shared__ double sp[];             // [Ls][SROW] (SMEM only)
   __shared__ double red_w[(QR_THREADS / 32) * NBMAX];
   __shared__ double red[NBMAX];
   __shared__ double piv[NBMAX];              // row j: W values (< j) and P values (>= j)
@@ -95,6 +97,8 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   const int64_t L = (R + G - 1) / G;
   const int64_t r0 = (int64_t)blockIdx.x * L;
   const int64_t r1 = min(R, r0 + L);
+  const int64_t rs = SMEM ? (HYB ? min(r1, r0 + Ls) : r1) : r0;   // rows [r0, rs) in shared memory
+  auto in_smem = [&](int64_t i) { return SMEM && i < rs; };
   if (tid == 0) s_gen = ld_acquire_gpu(bar);
   if (blockIdx.x == 0) {
     for (int64_t e = tid; e < wtop * nb; e += QR_THREADS) {   // rows above the sub-panel in W
@@ -104,8 +108,8 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     for (int e = tid; e < NBMAX * NBMAX; e += QR_THREADS) sT[e] = 0.0;
   }
   if constexpr (SMEM) {
-    for (int64_t e = tid; e < (r1 - r0) * nb; e += QR_THREADS) {
-      const int64_t il = e % (r1 - r0), c = e / (r1 - r0);
+    for (int64_t e = tid; e < (rs - r0) * nb; e += QR_THREADS) {
+      const int64_t il = e % (rs - r0), c = e / (rs - r0);
       sp[il * SROW + c] = P[cm(r0 + il, c, ldp)];
     }
   }
@@ -118,10 +122,11 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   for (int v = 0; v < NBMAX; ++v) acc[v] = 0.0;
   for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {        // column 0: rows i > 0
     if (i < 1) continue;
-    const double x0 = SMEM ? sp[(i - r0) * SROW] : P[cm(i, 0, ldp)];
+    const bool sm = in_smem(i);
+    const double x0 = sm ? sp[(i - r0) * SROW] : P[cm(i, 0, ldp)];
 #pragma unroll
     for (int p = 0; p < NBMAX; ++p)
-      if (p < nb) acc[p] += x0 * (SMEM ? sp[(i - r0) * SROW + p] : P[cm(i, p, ldp)]);
+      if (p < nb) acc[p] += x0 * (sm ? sp[(i - r0) * SROW + p] : P[cm(i, p, ldp)]);
   }
 
   // part: double-buffered by column parity; slot (buf, c) = CTA c's partial sums at [0, nb) and,
@@ -158,13 +163,13 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     const unsigned owner = (unsigned)(j / L);
     if (G == 1) {
       block_reduce_store<false>(acc, nb, red_w, red, 1);
-      if (tid < nb) piv[tid] = SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)];
+      if (tid < nb) piv[tid] = in_smem(j) ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)];
       t_column(j - 1, tj_prev);
       __syncthreads();
     } else {
       block_reduce_store<true>(acc, nb, red_w, pelem(buf, 0, blockIdx.x), (int)G);
       if (blockIdx.x == owner && tid < nb)
-        __stcg(pelem(buf, NBMAX + tid, owner), SMEM ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)]);
+        __stcg(pelem(buf, NBMAX + tid, owner), in_smem(j) ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)]);
       tr(j, 3);
 #ifdef UTV_QR_TRACE
       if (j == 5 && tid == 0 && blockIdx.x < 256) g_qr_arrive[blockIdx.x] = gtimer();
@@ -233,7 +238,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       // Rows in shared memory: the pivot columns are read and written with a runtime index, and
       // the reflector is applied to every column with the zero-padded swz (no per-column selects);
       // column j keeps its pre-scaling value in registers, so acc[j] is rescaled next column.
-      for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
+      for (int64_t i = r0 + tid; i < rs; i += QR_THREADS) {
         if (i < j) continue;
         double* srow = sp + (i - r0) * SROW;
         double row[NBMAX];
@@ -259,18 +264,21 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
         }
       }
       scal_prev = scal;
-      __syncthreads();
-      continue;
+      if constexpr (!HYB) {
+        __syncthreads();
+        continue;
+      }
     }
-    for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {
+    // rows in global memory (all of them, or the hybrid variant's tail); with SMEM the running sum
+    // of column j uses the pre-scaling x_j like the shared-memory rows (rescaled next column)
+    for (int64_t i = rs + tid; i < r1; i += QR_THREADS) {
       if (i < j) continue;                   // rows above the pivot: untouched
       // load the whole row first (all loads in flight; no shared-memory store in between that the
       // compiler would have to order them against), then compute, store and accumulate.  j is
       // runtime, so every index is static and selected with unrolled compares.
       double row[NBMAX];
 #pragma unroll
-      for (int c = 0; c < NBMAX; ++c)
-        row[c] = (c < nb) ? (SMEM ? sp[(i - r0) * SROW + c] : P[cm(i, c, ldp)]) : 0.0;
+      for (int c = 0; c < NBMAX; ++c) row[c] = (c < nb) ? P[cm(i, c, ldp)] : 0.0;
       double xj = 0.0, xj1 = 0.0, swj1 = 0.0;
 #pragma unroll
       for (int c = 0; c < NBMAX; ++c) {
@@ -289,15 +297,13 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       }
 #pragma unroll
       for (int c = 0; c < NBMAX; ++c)
-        if (c >= j && c < nb) {
-          if (SMEM) sp[(i - r0) * SROW + c] = row[c];
-          else P[cm(i, c, ldp)] = row[c];
-        }
+        if (c >= j && c < nb) P[cm(i, c, ldp)] = row[c];
       if (acc_next) {
 #pragma unroll
-        for (int c = 0; c < NBMAX; ++c) acc[c] += xn * row[c];
+        for (int c = 0; c < NBMAX; ++c) acc[c] += xn * ((SMEM && c == j) ? xj : row[c]);
       }
     }
+    if (SMEM) scal_prev = scal;
     __syncthreads();
   }
   t_column(nb - 1, tj_prev);                 // the last column of T
@@ -305,7 +311,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   // write back: P = R (upper) / 0 (below); W = explicit unit-lower Householder vectors
   for (int64_t e = tid; e < (r1 - r0) * nb; e += QR_THREADS) {
     const int64_t il = e % (r1 - r0), c = e / (r1 - r0), i = r0 + il;
-    const double x = SMEM ? sp[il * SROW + c] : P[cm(i, c, ldp)];
+    const double x = in_smem(i) ? sp[il * SROW + c] : P[cm(i, c, ldp)];
     P[cm(i, c, ldp)] = i <= c ? x : 0.0;
     W[cm(i, c, ldw)] = i < c ? 0.0 : (i == c ? 1.0 : x);
   }
@@ -341,25 +347,28 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
     static const int env_max = [] { const char* e = std::getenv("UTV_QR_MAXCTAS"); return e ? std::atoi(e) : 0; }();
     const int cap = g_qr_ctas > 0 ? g_qr_ctas : env_max;
     const int gmax = cap > 0 ? std::min(cap, pw.num_sms) : std::min(pw.num_sms, 160);
-    int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (R + 255) / 256));
-    // a CTA cap alone keeps the shared-memory variant (more CTAs if needed); forcing the global
-    // variant keeps G as chosen
-    if ((R + G - 1) / G > SMEM_ROWS_MAX && cap > 0 && !g_qr_force_global)
-      G = (int)std::min<int64_t>(pw.num_sms, (R + SMEM_ROWS_MAX - 1) / SMEM_ROWS_MAX);
+    const int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (R + 255) / 256));
     const int64_t Lr = (R + G - 1) / G;
-    const bool smem = Lr <= SMEM_ROWS_MAX && !g_qr_force_global;
+    // shared-memory rows: all of a CTA's rows, or (taller panels) the first SMEM_ROWS_MAX of them
+    // with the rest re-read from global memory / L2 per column (hybrid); the global-memory variant
+    // only when forced (UTV_TUNE_QR_GLOBAL)
+    const bool smem = !g_qr_force_global;
+    int64_t Ls = smem ? std::min<int64_t>(Lr, SMEM_ROWS_MAX) : 0;
     int64_t Rv = R; int nbv = nb; double* Pb = P + cm(jb, jb, ldp); double* Wb = W + cm(jb, jb, ldw);
     int64_t wtop = jb; double* taub = tau + jb; double* Tb = T + cm(jb, jb, ldt);
     void* args[] = {&Rv, &nbv, &Pb, (void*)&ldp, &Wb, (void*)&ldw, &wtop, &taub, &Tb, (void*)&ldt,
-                    (void*)&pw.part, (void*)&pw.bar};
+                    (void*)&pw.part, (void*)&pw.bar, &Ls};
     {
       ProfScope prof(st, kProfPanel, 1, 2.0 * (double)R * nb * nb, 16.0 * (double)R * nb);
-      prof.shape(R, nb, G, smem ? 1 : 0);                 // tag: 1 = shared-memory variant
+      // tag: 0 = global-memory variant, 1 = shared-memory variant, 3 = hybrid (smem head + global tail)
+      prof.shape(R, nb, G, !smem ? 0 : (Ls < Lr ? 3 : 1));
       static std::atomic<unsigned long long> attr{0};
       ensure_smem_attr(qr2_kernel<true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr);
-      const size_t smem_bytes = smem ? (size_t)Lr * SROW * sizeof(double) : 0;
-      UTV_CUDA(cudaLaunchCooperativeKernel(smem ? (void*)qr2_kernel<true> : (void*)qr2_kernel<false>, dim3(G),
-                                           dim3(QR_THREADS), args, smem_bytes, st));
+      static std::atomic<unsigned long long> attr_h{0};
+      ensure_smem_attr(qr2_kernel<true, true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr_h);
+      const size_t smem_bytes = smem ? (size_t)Ls * SROW * sizeof(double) : 0;
+      void* kern = !smem ? (void*)qr2_kernel<false> : (Ls < Lr ? (void*)qr2_kernel<true, true> : (void*)qr2_kernel<true>);
+      UTV_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(QR_THREADS), args, smem_bytes, st));
     }
     const int64_t wr = w - jb - nb;
     if (wr > 0) {

@@ -1159,6 +1159,30 @@ bool is_pinned_host_ptr(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Pins a host matrix for the DMA engines if the caller did not (unpinned when the object dies).
+struct HostPin {
+  void* p = nullptr;
+  void pin(double* A, int64_t m, int64_t n, int64_t lda) {
+    if (n <= 0 || is_pinned_host_ptr(A)) return;
+    UTV_CUDA(cudaHostRegister(A, ((size_t)(n - 1) * lda + m) * sizeof(double), cudaHostRegisterDefault));
+    p = A;
+  }
+  ~HostPin() { if (p) { cudaHostUnregister(p); cudaGetLastError(); } }
+};
+
+// The copy streams and events of the out-of-core mode (created once per handle).
+void ooc_streams(utv_handle h) {
+  if (h->h2d) return;
+  UTV_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+  UTV_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+  for (int s = 0; s < utv_handle_s::kStg; ++s) {
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_loaded[s], cudaEventDisableTiming));
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_free[s], cudaEventDisableTiming));
+  }
+  UTV_CUDA(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
+  UTV_CUDA(cudaEventCreateWithFlags(&h->ev_wb, cudaEventDisableTiming));
+}
+
 // utv_lstsq with UTV_HOST_STREAMED: A (host, overwritten by T), B / X host or device.
 int64_t lstsq_streamed(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
                        double* X, int64_t ldx, const utv_opts& opt) {
@@ -1167,25 +1191,9 @@ int64_t lstsq_streamed(utv_handle h, int64_t m, int64_t n, int64_t k, double* A,
     fail(UTV_ERR_UNSUPPORTED, "UTV_HOST_STREAMED is implemented for the fast option with factored V only");
   cudaStream_t st = h->stream;
   const int64_t b = opt.block;
-  // pin A for the DMA engines if the caller did not (unpinned for the duration of the call)
-  struct Pin {
-    void* p = nullptr;
-    ~Pin() { if (p) { cudaHostUnregister(p); cudaGetLastError(); } }
-  } pin;
-  if (!is_pinned_host_ptr(A)) {
-    UTV_CUDA(cudaHostRegister(A, ((size_t)(n - 1) * lda + m) * sizeof(double), cudaHostRegisterDefault));
-    pin.p = A;
-  }
-  if (!h->h2d) {
-    UTV_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
-    UTV_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
-    for (int s = 0; s < utv_handle_s::kStg; ++s) {
-      UTV_CUDA(cudaEventCreateWithFlags(&h->ev_loaded[s], cudaEventDisableTiming));
-      UTV_CUDA(cudaEventCreateWithFlags(&h->ev_free[s], cudaEventDisableTiming));
-    }
-    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
-    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_wb, cudaEventDisableTiming));
-  }
+  HostPin pin;
+  pin.pin(A, m, n, lda);
+  ooc_streams(h);
   h->ooc_h2d = h->ooc_d2h = 0;
   // fixed device memory: workspace, factored V, then the OOC arena (C, X, diag, panel, staging)
   Ctx c = make_ctx(h, m, n, k, b);
@@ -1566,6 +1574,301 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   return r;
 }
 
+// ------------------------------------------------------------------------------------------
+// Multi-GPU x out-of-core (SURVEY 8(e) with 8(f) #1; the north star's cfg5: "tiles streamed from
+// pinned host memory across 8 x B200"): each rank's block-cyclic shard (m x nloc) stays in ITS
+// pinned host memory and is overwritten by its shard of T there; HBM holds the rank's workspace,
+// the replicated factored V, a staging ring and as many of its LAST local column blocks as the
+// device budget allows (utv_set_device_budget), exactly as factor_ooc on one GPU.  The collectives
+// are those of lstsq_dist (AllReduce Z / X, AllGather Y, Broadcast W_U / T_U / U_s / V_s / sigma);
+// per step the rank streams its trailing columns 2q + 2 times and writes them back once (the
+// right update of all rows, the deferred U_s^T of the previous block, Q_U^T, and the next step's
+// local sketch product in one read+write pass).  The SVD of block i (owner's side stream) is
+// applied one step later (lag 1, folded into the next step's pass, as on one GPU).
+// ------------------------------------------------------------------------------------------
+
+// The rank's out-of-core arena (two panel buffers, the staging ring, the resident last blocks),
+// sized under the device budget; all device allocations happen here, before the ranks agree.
+void dist_ooc_prepare(utv_handle h, Ooc& o, int64_t m, int64_t n, int64_t k, double* A, int64_t lda,
+                      const utv_opts& opt) {
+  const int P = h->comm->nranks, p = h->comm->rank;
+  const int64_t b = opt.block, nloc = dist_local_cols(n, b, P, p);
+  dist_reserve(h, m, n, k, opt);
+  ooc_streams(h);
+  h->ooc_h2d = h->ooc_d2h = 0;
+  static const int64_t chunk_blocks = [] {
+    const char* e = std::getenv("UTV_OOC_CHUNK_BLOCKS");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : (int64_t)4;
+  }();
+  const int64_t cw = std::max<int64_t>(b, std::min<int64_t>(chunk_blocks * b, (nloc + b - 1) / b * b));
+  const size_t fixed = 2 * (size_t)m * b + (size_t)utv_handle_s::kStg * m * cw + 64;
+  size_t free_b = 0, total_b = 0;
+  UTV_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t used_b = (h->ws_doubles + h->vbuf_doubles + h->dbuf_doubles + h->ooc_doubles) * sizeof(double);
+  size_t avail = free_b + h->ooc_doubles * sizeof(double);
+  avail = avail > ((size_t)1 << 30) ? avail - ((size_t)1 << 30) : 0;
+  if (h->dev_budget > 0) {
+    const size_t base = used_b - h->ooc_doubles * sizeof(double);
+    avail = std::min(avail, (size_t)h->dev_budget > base ? (size_t)h->dev_budget - base : (size_t)0);
+  }
+  if (avail < fixed * sizeof(double))
+    fail(UTV_ERR_ALLOC, "device budget too small for the streamed working set of this rank");
+  int64_t res_cols = (int64_t)((avail / sizeof(double) - fixed) / (size_t)m);
+  if (const char* e = std::getenv("UTV_OOC_MAX_RESIDENT_COLS"))
+    res_cols = std::min<int64_t>(res_cols, std::max<int64_t>(0, std::atoll(e)));
+  o = Ooc{};
+  o.h = h; o.m = m; o.n = nloc; o.b = b; o.hA = A; o.lda = lda; o.cw = cw;
+  o.c_res = res_cols >= nloc ? 0 : std::min<int64_t>(nloc, (nloc - res_cols + b - 1) / b * b);
+  const size_t total = fixed + (size_t)m * (nloc - o.c_res);
+  if (h->ooc_doubles < total) {
+    if (h->ooc) { UTV_CUDA(cudaFree(h->ooc)); h->ooc = nullptr; h->ooc_doubles = 0; }
+    ensure_buf(&h->ooc, &h->ooc_doubles, total);
+  }
+  double* q = h->ooc;
+  o.pb[0] = q; q += (size_t)m * b;
+  o.pb[1] = q; q += (size_t)m * b;
+  for (int s = 0; s < utv_handle_s::kStg; ++s) { o.stg[s] = q; q += (size_t)m * cw; }
+  o.res = q;
+  h->ooc_resident_cols = nloc - o.c_res;
+}
+
+// a9 on a block-cyclic T kept in the ranks' host memory: dist_solve_z with the owner's T column
+// block fetched (rows 0:j1) through the out-of-core arena.
+void dist_solve_z_ooc(const Ctx& c, Comm& comm, Ooc& o, int64_t r, int64_t b, const double* Cm, int64_t ldc,
+                      int64_t k) {
+  if (r <= 0 || k <= 0) return;
+  cudaStream_t st = c.st;
+  const int P = comm.nranks, p = comm.rank;
+  double* Zb = c.at(c.L.zsolve);
+  double* Sp = c.at(c.L.nY);
+  double* D = c.at(c.L.R);
+  double* sbuf = c.at(c.L.tmp);
+  double* zb = c.at(c.L.tmp2);
+  launch_set_zero(st, r, k, Sp, r);
+  for (int64_t blk = (r - 1) / b; blk >= 0; --blk) {
+    const int64_t j0 = blk * b, j1 = std::min(r, j0 + b), w = j1 - j0;
+    const int o_ = (int)(blk % P);
+    launch_copy(st, w, k, Sp + j0, r, sbuf, w);
+    comm.allreduce(sbuf, (size_t)w * k, st);
+    if (p == o_) {
+      const int64_t lc = (blk / P) * b;
+      int64_t ldt = o.m;
+      const double* Tb = ooc_block(o, c, lc, w, j1, &ldt);
+      launch_copy(st, w, k, Cm + j0, ldc, zb, w);
+      launch_axpy(st, w * k, -1.0, sbuf, zb);
+      launch_copy(st, w, w, Tb + j0, ldt, D, b);
+      launch_trsv_block(st, 0, w, D, b, zb, w, k);
+      if (j0 > 0) c.gemm(false, false, j0, k, w, 1.0, Tb, ldt, zb, w, 1.0, Sp, r);
+    }
+    comm.bcast(zb, (size_t)w * k, o_, st);
+    launch_copy(st, w, k, zb, w, Zb + j0, r);
+  }
+}
+
+int64_t lstsq_dist_ooc(utv_handle h, Ooc& o, int64_t m, int64_t n, int64_t k, double* B, int64_t ldb, double* X,
+                       int64_t ldx, const utv_opts& opt) {
+  Comm& comm = *h->comm;
+  const int P = comm.nranks, p = comm.rank;
+  const int64_t b = opt.block, nb = (n + b - 1) / b, nloc = o.n;
+  cudaStream_t st = h->stream;
+  const int ns = h->num_sms;
+  Ctx c = make_ctx(h, m, n, k, b);
+  const Layout& L = c.L;
+  const size_t wdbl = factored_w_doubles(n, b), tdbl = (size_t)nb * b * b;
+  FactoredV fv;
+  fv.W = h->vbuf; fv.T = h->vbuf + wdbl; fv.Vs = fv.T + tdbl;
+  const int64_t Lmax = (nb + P - 1) / P * b;
+  const size_t kk = (size_t)std::max<int64_t>(k, 1);
+  double* Ypad = h->dbuf;
+  double* recv = Ypad + (size_t)Lmax * b;
+  double* dg = recv + (size_t)P * Lmax * b;
+  double* sbuf = dg + n + 64;
+  double* zb = sbuf + (size_t)b * kk;
+  double* flags = zb + (size_t)b * kk;
+  double* usring = flags + 64;
+  double* sgring = usring + (size_t)(utv_handle_s::kLagMax + 1) * b * b;
+  UTV_CUDA(cudaMemsetAsync(h->info, 0, 4 * sizeof(int), st));
+  UTV_CUDA(cudaMemsetAsync(h->flag, 0, sizeof(int), st));
+  if (k > 0) launch_check_finite(st, m, k, B, ldb, h->flag);
+  double *G = c.at(L.G), *Y = c.at(L.Y), *Z = c.at(L.Z), *WP = c.at(L.Wv), *Xa = c.at(L.X), *LU = c.at(L.Wu);
+  double *Tu = c.at(L.Tu), *tauu = c.at(L.tauu), *tauv = c.at(L.tauv), *Z1 = c.at(L.Z1), *Z2 = c.at(L.Z2);
+  double *Yl = c.at(L.tmp), *tmp = c.at(L.tmp2);
+  double* X2 = LU;
+  if (o.c_res < nloc) {                                              // resident local blocks: loaded once
+    UTV_CUDA(cudaEventRecord(h->ev_done, st));
+    UTV_CUDA(cudaStreamWaitEvent(h->h2d, h->ev_done, 0));
+    ooc_load(o, c, o.res, m, 0, m, o.c_res, nloc - o.c_res, h->ev_loaded[0]);
+    launch_check_finite(st, m, nloc - o.c_res, o.res, m, h->flag);
+  }
+  bool y_ready = false;
+  bool fin = false;                                                  // block i-1's SVD results pending
+  int64_t f_i = 0, f_j0 = 0, f_bw = 0, f_lt = 0;
+  int f_owner = 0;
+  auto slot_us = [&](int64_t i) { return usring + (size_t)(i % (utv_handle_s::kLagMax + 1)) * b * b; };
+  auto slot_sg = [&](int64_t i) { return sgring + (size_t)(i % (utv_handle_s::kLagMax + 1)) * b; };
+  // the SVD results of block i-1 (f_*): broadcast; diag(T); C1 := U_s^T C1; on its owner the block
+  // is finalised (A11 := Sigma, A01 := A01 V_s) and written back from panel buffer (f_i & 1)
+  auto finalize = [&]() {
+    double* Usp = slot_us(f_i);
+    double* sgp = slot_sg(f_i);
+    double* Vsp = fv.Vs + (size_t)f_i * b * b;
+    if (p == f_owner) UTV_CUDA(cudaStreamWaitEvent(st, h->ev_svd, 0));
+    comm.bcast(Usp, (size_t)b * b, f_owner, st);
+    comm.bcast(Vsp, (size_t)b * b, f_owner, st);
+    comm.bcast(sgp, (size_t)b, f_owner, st);
+    launch_copy(st, f_bw, 1, sgp, f_bw, dg + f_j0, n);
+    if (p == f_owner) {
+      const bool resident = f_lt >= o.c_res;
+      double* Af = resident ? o.res + cm(0, f_lt - o.c_res, m) : o.pb[f_i & 1];
+      launch_set_diag(st, f_bw, sgp, Af + f_j0, m);
+      if (f_j0 > 0) {
+        c.gemm(false, false, f_j0, f_bw, f_bw, 1.0, Af, m, Vsp, b, 0.0, tmp, f_j0);
+        launch_copy(st, f_j0, f_bw, tmp, f_j0, Af, m);
+      }
+      ooc_block_store(o, c, f_lt, f_bw, (int)(f_i & 1));
+    }
+    if (k > 0) {
+      c.gemm(true, false, f_bw, k, f_bw, 1.0, Usp, b, B + f_j0, ldb, 0.0, Z1, f_bw);
+      launch_copy(st, f_bw, k, Z1, f_bw, B + f_j0, ldb);
+    }
+  };
+  for (int64_t i = 0, j0 = 0; i < nb; ++i, j0 += b) {
+    const int64_t bw = std::min(b, n - j0), mp = m - j0, np = n - j0;
+    const int owner = (int)(i % P);
+    const bool own = p == owner;
+    const int64_t first = i <= p ? 0 : (i - p + P - 1) / P;
+    const int64_t lt = first * b, ncl = nloc - lt;
+    const int64_t lr = lt + (own ? bw : 0), nrl = ncl - (own ? bw : 0);
+    const int64_t ldwp = std::max<int64_t>(ncl, 1);
+    const bool right = np > b;
+    double* Wu = LU + cm(j0, b, m);
+    double* Tvs = fv.T + (size_t)i * b * b;
+    if (right) {
+      if (!y_ready) {                                                  // a1 + local Y = A'^T G
+        launch_sketch(st, opt.seed, i, j0, mp, b, G, mp, ns);
+        ooc_pass(o, c, lt, j0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+          if (i == 0 && col < o.c_res) launch_check_finite(st, mp, w, d, ld, h->flag);
+          c.gemm(true, false, w, b, mp, 1.0, d, ld, G, mp, 0.0, Yl + (col - lt), ldwp);
+        });
+      }
+      for (int32_t it = 0; it < opt.power_iters; ++it) {              // a2 (R7)
+        launch_set_zero(st, mp, b, Z, mp);
+        ooc_pass(o, c, lt, j0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+          c.gemm(false, false, mp, b, w, 1.0, d, ld, Yl + (col - lt), ldwp, 1.0, Z, mp);
+        });
+        comm.allreduce(Z, (size_t)mp * b, st);
+        ooc_pass(o, c, lt, j0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+          c.gemm(true, false, w, b, mp, 1.0, d, ld, Z, mp, 0.0, Yl + (col - lt), ldwp);
+        });
+      }
+      launch_copy(st, ncl, b, Yl, ldwp, Ypad, Lmax);                   // AllGather(Y)
+      comm.allgather(Ypad, recv, (size_t)Lmax * b, st);
+      launch_assemble_y(st, np, b, b, i, P, Lmax, recv, Y, np);
+      fv.woff.push_back(fv.woff.empty() ? 0 : fv.woff.back() + (size_t)fv.np.back() * b);
+      fv.j0.push_back(j0); fv.np.push_back(np); fv.has_q.push_back(1);
+      double* Wv = fv.W + fv.woff.back();
+      panel_qr(st, np, b, Y, np, Wv, np, tauv, Tvs, b, c.pw);          // a3 (same on every rank)
+      launch_gather_local(st, ncl, b, b, i, P, p, Wv, np, WP, ldwp);
+      launch_set_zero(st, m, b, Xa, m);                                // a4, R1: X = A W_V, all rows
+      ooc_pass(o, c, lt, 0, false, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+        c.gemm(false, false, m, b, w, 1.0, d, ld, WP + (col - lt), ldwp, 1.0, Xa, m);
+      });
+      comm.allreduce(Xa, (size_t)m * b, st);
+      c.gemm(false, false, m, b, b, 1.0, Xa, m, Tvs, b, 0.0, X2, m);
+    }
+    // block i on its owner: right update (all rows), the previous block's U_s^T on its rows
+    int64_t lda_i = m;
+    double* Ai = nullptr;
+    if (own) {
+      Ai = ooc_block(o, c, lt, bw, m, &lda_i, (int)(i & 1));
+      if (i == 0 && !right && lt < o.c_res) launch_check_finite(st, m, bw, Ai, lda_i, h->flag);
+      if (right) c.gemm(false, true, m, bw, b, -1.0, X2, m, WP, ldwp, 1.0, Ai, lda_i);
+    }
+    bool us_pend = false;
+    const double* Usp = nullptr;
+    int64_t pj0 = 0, pbw = 0;
+    if (fin) {
+      finalize();
+      Usp = slot_us(f_i); pj0 = f_j0; pbw = f_bw;
+      if (own) {                                                       // block i's part of A12(i-1)
+        c.gemm(true, false, pbw, bw, pbw, 1.0, Usp, b, Ai + pj0, lda_i, 0.0, Z1, pbw);
+        launch_copy(st, pbw, bw, Z1, pbw, Ai + pj0, lda_i);
+      }
+      us_pend = nrl > 0;
+      fin = false;
+    }
+    // a5 on the owner; Broadcast(W_U) of the live rows (packed), T_U
+    if (own) {
+      panel_qr(st, mp, bw, Ai + j0, lda_i, Wu, m, tauu, Tu, b, c.pw);
+      launch_copy(st, mp, bw, Wu, m, Xa, mp);
+    }
+    comm.bcast(Xa, (size_t)mp * bw, owner, st);
+    if (!own) launch_copy(st, mp, bw, Xa, mp, Wu, m);
+    comm.bcast(Tu, (size_t)b * b, owner, st);
+    if (k > 0) {                                                       // C := Q_U^T C
+      double* Cr = B + j0;
+      c.gemm(true, false, bw, k, mp, 1.0, Wu, m, Cr, ldb, 0.0, Z1, bw);
+      c.gemm(true, false, bw, k, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+      c.gemm(false, false, mp, k, bw, -1.0, Wu, m, Z2, bw, 1.0, Cr, ldb);
+    }
+    if (own) {                                                         // a7 on the side stream
+      UTV_CUDA(cudaEventRecord(h->ev_panel, st));
+      UTV_CUDA(cudaStreamWaitEvent(c.side, h->ev_panel, 0));
+      svd_small(c.side, bw, Ai + j0, lda_i, slot_us(i), b, slot_sg(i), fv.Vs + (size_t)i * b * b, b, c.sw);
+      UTV_CUDA(cudaEventRecord(h->ev_svd, c.side));
+    }
+    // one read+write pass over this rank's columns > block i (+ the next step's local sketch)
+    const bool next_sketch = np - bw > b;                              // the same on every rank
+    if (next_sketch) launch_sketch(st, opt.seed, i + 1, j0 + b, mp - b, b, G, mp - b, ns);
+    const int64_t ldwn = std::max<int64_t>(nrl, 1);                    // next step's local Y
+    if (nrl > 0) {
+      ooc_pass(o, c, lr, 0, true, [&](double* d, int64_t ld, int64_t col, int64_t w) {
+        if (right) c.gemm(false, true, m, w, b, -1.0, X2, m, WP + (col - lt), ldwp, 1.0, d, ld);
+        if (us_pend) {                                                 // A12(i-1) := U_s^T A12
+          c.gemm(true, false, pbw, w, pbw, 1.0, Usp, b, d + pj0, ld, 0.0, Z1, pbw);
+          launch_copy(st, pbw, w, Z1, pbw, d + pj0, ld);
+        }
+        double* dr = d + j0;                                           // a6, R3
+        c.gemm(true, false, bw, w, mp, 1.0, Wu, m, dr, ld, 0.0, Z1, bw);
+        c.gemm(true, false, bw, w, bw, 1.0, Tu, b, Z1, bw, 0.0, Z2, bw);
+        c.gemm(false, false, mp, w, bw, -1.0, Wu, m, Z2, bw, 1.0, dr, ld);
+        if (next_sketch)
+          c.gemm(true, false, w, b, mp - b, 1.0, d + j0 + b, ld, G, mp - b, 0.0, Yl + (col - lr), ldwn);
+      });
+    }
+    y_ready = next_sketch;
+    fin = true;
+    f_i = i; f_j0 = j0; f_bw = bw; f_lt = lt; f_owner = owner;
+  }
+  if (fin) finalize();                                                 // the last block
+  UTV_CUDA(cudaMemcpyAsync(h->h_info, h->info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  UTV_CUDA(cudaMemcpyAsync(h->h_info + 2, h->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  comm.wait(st);
+  const double fl[2] = {(double)h->h_info[2], (double)h->h_info[1]};
+  UTV_CUDA(cudaMemcpyAsync(flags, fl, sizeof(fl), cudaMemcpyHostToDevice, st));
+  comm.allreduce(flags, 2, st);
+  double flo[2] = {0.0, 0.0};
+  UTV_CUDA(cudaMemcpyAsync(flo, flags, sizeof(flo), cudaMemcpyDeviceToHost, st));
+  comm.wait(st);
+  h->agreed_failure = flo[0] != 0.0 || flo[1] != 0.0;
+  if (flo[0] != 0.0) fail(UTV_ERR_NUMERICAL, "NaN or Inf in A or B (on some rank)");
+  if (flo[1] != 0.0) fail(UTV_ERR_NUMERICAL, "Jacobi SVD of a diagonal block did not converge in 30 sweeps");
+  const int64_t r = finish_factor(c, n, dg, 0, opt.tau, true);        // a8 (replicated diag)
+  if (k > 0) {
+    dist_solve_z_ooc(c, comm, o, r, b, B, ldb, k);                     // a9
+    solve_factored(c, n, r, nullptr, 0, nullptr, 0, k, X, ldx, fv, b, nullptr, true);
+  }
+  if (o.c_res < nloc) {                                                // resident part of the shard of T
+    UTV_CUDA(cudaEventRecord(h->ev_done, st));
+    UTV_CUDA(cudaStreamWaitEvent(h->d2h, h->ev_done, 0));
+    copy2d(h->d2h, o.hA + cm(0, o.c_res, o.lda), o.lda, o.res, m, m, nloc - o.c_res, cudaMemcpyDeviceToHost);
+    h->ooc_d2h += (nloc - o.c_res) * m * 8;
+  }
+  UTV_CUDA(cudaStreamSynchronize(h->d2h));
+  comm.wait(st);
+  return r;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1883,26 +2186,40 @@ utv_status utv_lstsq(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, i
       // fails the call on every rank instead of leaving the peers blocked in a collective.
       utv_status local = UTV_OK;
       std::string msg;
+      const bool streamed = opts && (opts->flags & UTV_HOST_STREAMED);
+      HostPin pin;                                                     // streamed: the shard, pinned
+      Ooc o;
       try {
         check_opts(opts);
         if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
         if (m < n) fail(UTV_ERR_SHAPE, "m < n: single-GPU in-core utv_lstsq only (R21)");
-        if (opts->flags & (UTV_NULLIFY_T12 | UTV_EXPLICIT_V | UTV_HOST_STREAMED))
+        if (opts->flags & (UTV_NULLIFY_T12 | UTV_EXPLICIT_V))
           fail(UTV_ERR_UNSUPPORTED, "the multi-GPU path implements the fast option with factored V only");
+        if (streamed && (opts->flags & UTV_KEEP_FACTORS))
+          fail(UTV_ERR_UNSUPPORTED, "UTV_KEEP_FACTORS with UTV_HOST_STREAMED");
         check_ld("lda", lda, m);
         if (k > 0) { check_ld("ldb", ldb, m); check_ld("ldx", ldx, n); }
         const int64_t nloc = n > 0 ? dist_local_cols(n, opts->block, h->comm->nranks, h->comm->rank) : 0;
         if ((nloc > 0 && !A) || (k > 0 && (!B || !X))) fail(UTV_ERR_ARG, "NULL matrix");
-        if ((nloc > 0 && !is_device_ptr(A)) || (k > 0 && (!is_device_ptr(B) || !is_device_ptr(X))))
-          fail(UTV_ERR_ARG, "the multi-GPU path takes device pointers (A = this rank's shard)");
-        if (n > 0) dist_reserve(h, m, n, k, *opts);
+        if (k > 0 && (!is_device_ptr(B) || !is_device_ptr(X)))
+          fail(UTV_ERR_ARG, "the multi-GPU path takes device B and X (replicated)");
+        if (nloc > 0 && streamed == is_device_ptr(A))
+          fail(UTV_ERR_ARG, streamed ? "UTV_HOST_STREAMED: A (this rank's shard) must be in host memory"
+                                     : "the multi-GPU path takes a device A (this rank's shard)");
+        if (n > 0 && streamed) {
+          pin.pin(A, m, nloc, lda);
+          dist_ooc_prepare(h, o, m, n, k, A, lda, *opts);
+        } else if (n > 0) {
+          dist_reserve(h, m, n, k, *opts);
+        }
       } catch (const ApiError& e) {
         local = e.st;
         msg = e.msg;
       }
       dist_agree(h, local, msg);
       if (n == 0) { if (rank) *rank = 0; return; }
-      const int64_t r = lstsq_dist(h, m, n, k, A, lda, B, ldb, X, ldx, *opts);
+      const int64_t r = streamed ? lstsq_dist_ooc(h, o, m, n, k, B, ldb, X, ldx, *opts)
+                                 : lstsq_dist(h, m, n, k, A, lda, B, ldb, X, ldx, *opts);
       if (rank) *rank = r;
       return;
     }
