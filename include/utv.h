@@ -71,8 +71,11 @@ utv_status utv_create(utv_handle* handle, int device, void* stream);
  * Sigma on the diagonal blocks it owns); B (m x k, device) is replicated on every rank and overwritten by
  * U^T B; X (n x k, device) is written, identical on every rank; *rank is identical on every rank.
  * All ranks must make the same calls with the same m, n, k, opts (collectives in lock step).
- * Fast option with factored V only (UTV_NULLIFY_T12 / UTV_EXPLICIT_V / UTV_HOST_STREAMED ->
- * UTV_ERR_UNSUPPORTED); utv_factor on such a handle -> UTV_ERR_UNSUPPORTED.
+ * Fast option with factored V only (UTV_NULLIFY_T12 / UTV_EXPLICIT_V -> UTV_ERR_UNSUPPORTED);
+ * utv_factor on such a handle -> UTV_ERR_UNSUPPORTED.  With UTV_HOST_STREAMED the shard A is in
+ * HOST memory (pinned, or registered for the call) and is streamed through the rank's device
+ * (out-of-core x multi-GPU, SURVEY 8(e) x 8(f) #1; the device budget is per handle); B, X stay on
+ * the device.
  * Failures: the ranks first agree on the call (one AllReduce of a flag after every rank has checked
  * its arguments and reserved its device memory), so a rank-local argument / allocation error fails
  * the call on EVERY rank (the peers get UTV_ERR_ARG) and the handle stays usable; NaN / Inf and
@@ -97,6 +100,25 @@ utv_status utv_create_dist(utv_handle* handle, int device, void* stream, const v
  * forever, and the group stays unusable (destroy it).  Destroy each handle with utv_destroy. */
 utv_status utv_create_local_group(utv_handle* handles, int nranks, const int* devices,
                                   void* const* streams);
+
+/* A caller-supplied communicator ("bring your own": MPI, gloo through torch.distributed, ...) for
+ * the same multi-GPU algorithm.  Every callback is invoked on the calling host thread in the rank's
+ * program order (the same order on every rank); buffers are device pointers on the handle's device
+ * and `stream` (a cudaStream_t) orders them: the callback must make its result visible in stream
+ * order (e.g. synchronise the stream, exchange, copy back) and return 0, or non-zero on failure
+ * (the call then fails with UTV_ERR_NCCL).  allreduce_sum: in-place elementwise sum of `count`
+ * doubles over the ranks, the SAME result on every rank; broadcast: `count` doubles from `root`;
+ * allgather: recv[r * count + i] = send of rank r.  abort (may be NULL) is called when this rank
+ * fails inside the method's collectives, so that the peers stop waiting.  `ops` is copied. */
+typedef struct {
+  int (*allreduce_sum)(void* ctx, double* buf, int64_t count, void* stream);
+  int (*broadcast)(void* ctx, double* buf, int64_t count, int root, void* stream);
+  int (*allgather)(void* ctx, const double* send, double* recv, int64_t count, void* stream);
+  void (*abort)(void* ctx);
+  void* ctx;
+} utv_comm_ops;
+utv_status utv_create_with_comm(utv_handle* handle, int device, void* stream, int nranks, int rank,
+                                const utv_comm_ops* ops);
 
 /* Number of columns of rank `rank`'s shard of an n-column matrix (block-cyclic, block `block`). */
 int64_t utv_dist_local_cols(int64_t n, int64_t block, int nranks, int rank);

@@ -28,13 +28,25 @@ EXPORTED = ["utv_create", "utv_create_dist", "utv_destroy", "utv_last_error", "u
             "utv_svd_small", "utv_gemm", "utv_rank", "utv_profile", "utv_profile_read",
             "utv_profile_dump", "utv_svd_block", "utv_svd_status", "utv_trsm_upper",
             "utv_rank_diag", "utv_set_device_budget", "utv_stream_stats", "utv_get_unique_id",
-            "utv_create_local_group", "utv_dist_local_cols", "utv_tune", "utv_solve_rhs"]
+            "utv_create_local_group", "utv_dist_local_cols", "utv_tune", "utv_solve_rhs",
+            "utv_create_with_comm"]
 PROF_FAMILIES = ["gemm", "panel", "svd", "sketch", "solve", "misc"]
 
 
 class _ProfEntry(C.Structure):
     _fields_ = [("launches", C.c_int64), ("calls", C.c_int64), ("ms", C.c_double), ("flops", C.c_double),
                 ("bytes", C.c_double)]
+
+
+_AR_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+_BC_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p)
+_AG_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+_AB_CB = C.CFUNCTYPE(None, C.c_void_p)
+
+
+class _CommOps(C.Structure):
+    _fields_ = [("allreduce_sum", _AR_CB), ("broadcast", _BC_CB), ("allgather", _AG_CB), ("abort", _AB_CB),
+                ("ctx", C.c_void_p)]
 
 
 class UtvError(RuntimeError):
@@ -104,6 +116,7 @@ def lib() -> C.CDLL:
             "utv_stream_stats": ([p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], st),
             "utv_tune": ([C.c_int, i64, C.POINTER(i64)], st),
             "utv_solve_rhs": ([p, i64, i64, i64, p, i64, p, i64, p, i64, C.POINTER(i64)], st),
+            "utv_create_with_comm": ([C.POINTER(p), C.c_int, p, C.c_int, C.c_int, C.POINTER(_CommOps)], st),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -391,6 +404,104 @@ def dist_handle(nccl_uid: bytes, nranks: int, rank: int, device: int | None = No
     if st != UTV_OK:
         raise UtvError(st, "utv_create_dist failed")
     return Handle._wrap(h, device, stream)
+
+
+def _cudart():
+    """The CUDA runtime torch already loaded (cudaMemcpy / cudaStreamSynchronize for host staging)."""
+    global _cudart_lib
+    if _cudart_lib is None:
+        import glob
+        import os as _os
+        cands = ["libcudart.so.12", "libcudart.so"]
+        for d in (_os.path.join(_os.path.dirname(torch.__file__), "lib"),):
+            cands += sorted(glob.glob(_os.path.join(d, "libcudart*.so*")))
+        try:
+            import nvidia.cuda_runtime as _ncr
+            cands += sorted(glob.glob(_os.path.join(list(_ncr.__path__)[0], "lib", "libcudart.so*")))
+        except Exception:
+            pass
+        err = None
+        for c in cands:
+            try:
+                _cudart_lib = C.CDLL(c)
+                break
+            except OSError as e:
+                err = e
+        if _cudart_lib is None:
+            raise RuntimeError(f"libcudart not found: {err}")
+        _cudart_lib.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+        _cudart_lib.cudaStreamSynchronize.argtypes = [C.c_void_p]
+    return _cudart_lib
+
+
+_cudart_lib = None
+
+
+def comm_handle(rank: int, nranks: int, group=None, device: int | None = None) -> Handle:
+    """Rank `rank` of a multi-GPU handle whose collectives go through torch.distributed on `group`
+    (utv_create_with_comm; e.g. gloo, one process per rank).  The device buffers are staged through
+    host memory in the callbacks (argument marshalling; the method's arithmetic stays in libutv)."""
+    import numpy as np
+    import torch.distributed as tdist
+    device = torch.cuda.current_device() if device is None else int(device)
+    stream = torch.cuda.current_stream(device)
+    rt = _cudart()
+    H2D, D2H = 1, 2
+
+    def stage_out(buf, n, st):
+        rt.cudaStreamSynchronize(C.c_void_p(st))
+        a = np.empty(n, dtype=np.float64)
+        if rt.cudaMemcpy(a.ctypes.data, buf, n * 8, D2H) != 0:
+            raise RuntimeError("cudaMemcpy D2H failed")
+        return a
+
+    def stage_in(buf, a):
+        if rt.cudaMemcpy(buf, a.ctypes.data, a.size * 8, H2D) != 0:
+            raise RuntimeError("cudaMemcpy H2D failed")
+
+    def ar(ctx, buf, n, st):
+        try:
+            a = stage_out(buf, n, st)
+            t = torch.from_numpy(a)
+            tdist.all_reduce(t, group=group)
+            stage_in(buf, a)
+            return 0
+        except Exception:               # noqa: BLE001 -- reported to libutv as a failed collective
+            return 1
+
+    def bc(ctx, buf, n, root, st):
+        try:
+            a = stage_out(buf, n, st)
+            t = torch.from_numpy(a)
+            tdist.broadcast(t, src=tdist.get_global_rank(group, root) if group is not None else root, group=group)
+            if rank != root:
+                stage_in(buf, a)
+            return 0
+        except Exception:               # noqa: BLE001
+            return 1
+
+    def ag(ctx, send, recv, n, st):
+        try:
+            a = torch.from_numpy(stage_out(send, n, st))
+            outs = [torch.empty(n, dtype=torch.float64) for _ in range(nranks)]
+            tdist.all_gather(outs, a, group=group)
+            stage_in(recv, torch.cat(outs).numpy())
+            return 0
+        except Exception:               # noqa: BLE001
+            return 1
+
+    def ab(ctx):
+        pass
+
+    cbs = (_AR_CB(ar), _BC_CB(bc), _AG_CB(ag), _AB_CB(ab))
+    ops = _CommOps(cbs[0], cbs[1], cbs[2], cbs[3], None)
+    h = C.c_void_p()
+    st = lib().utv_create_with_comm(C.byref(h), device, C.c_void_p(stream.cuda_stream), nranks, rank, C.byref(ops))
+    if st != UTV_OK:
+        raise UtvError(st, "utv_create_with_comm failed")
+    hd = Handle._wrap(h, device, stream)
+    hd._callbacks = cbs                # the C function pointers must outlive the handle
+    return hd
 
 
 def local_group(nranks: int, devices=None, streams=None) -> list:

@@ -238,6 +238,25 @@ struct LocalComm : Comm {
   }
 };
 
+// Caller-supplied communicator (utv_create_with_comm): the collectives are forwarded to host
+// callbacks in program order; a non-zero return fails the call.
+struct CallbackComm : Comm {
+  utv_comm_ops ops{};
+  void check(int rc, const char* what) {
+    if (rc != 0) throw CommError{std::string("user communicator: ") + what + " returned " + std::to_string(rc)};
+  }
+  void abort() override { if (ops.abort) ops.abort(ops.ctx); }
+  void allreduce(double* buf, size_t n, cudaStream_t st) override {
+    if (n) check(ops.allreduce_sum(ops.ctx, buf, (int64_t)n, st), "allreduce_sum");
+  }
+  void bcast(double* buf, size_t n, int root, cudaStream_t st) override {
+    if (n) check(ops.broadcast(ops.ctx, buf, (int64_t)n, root, st), "broadcast");
+  }
+  void allgather(const double* send, double* recv, size_t n, cudaStream_t st) override {
+    if (n) check(ops.allgather(ops.ctx, send, recv, (int64_t)n, st), "allgather");
+  }
+};
+
 // Factored V: instead of accumulating V explicitly (2 n^3 flops at square
 // shapes, 23% of the work at q = 2), keep every step's block reflector (W_V, T_V) and V_s:
 //   V = Q_1 Q_2 ... Q_s D_1 ... D_s   (D_i = V_s on block i commutes with Q_j, j > i: H5),
@@ -1957,6 +1976,25 @@ utv_status utv_create_dist(utv_handle* handle, int device, void* stream, const v
     utv_destroy(h);
     return s;
   }
+  *handle = h;
+  return UTV_OK;
+}
+
+utv_status utv_create_with_comm(utv_handle* handle, int device, void* stream, int nranks, int rank,
+                                const utv_comm_ops* ops) {
+  if (!handle) return UTV_ERR_ARG;
+  *handle = nullptr;
+  if (!ops || !ops->allreduce_sum || !ops->broadcast || !ops->allgather || nranks < 1 || rank < 0 || rank >= nranks)
+    return UTV_ERR_ARG;
+  utv_handle h = nullptr;
+  utv_status s = utv_create(&h, device, stream);
+  if (s != UTV_OK) return s;
+  auto* c = new (std::nothrow) CallbackComm();
+  if (!c) { utv_destroy(h); return UTV_ERR_ALLOC; }
+  c->ops = *ops;
+  c->nranks = nranks;
+  c->rank = rank;
+  h->comm = c;
   *handle = h;
   return UTV_OK;
 }
