@@ -30,6 +30,13 @@ __device__ __forceinline__ void cluster_barrier() {
                "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void dmma16884(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
 __device__ __forceinline__ double warp_sum_bcast(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -42,6 +49,7 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
   extern __shared__ __align__(16) double jsm[];
   double* sW = jsm;
   double* sJ = jsm + 2 * JBLK * bw;
+  __shared__ double sQ[2 * JBLK * (2 * JBLK + 1)];   // this round's rotations, column c at sQ + c*33
   __shared__ int s_gcol[2 * JBLK];
   __shared__ int s_rot;
   __shared__ double s_nrm[2 * JBLK];
@@ -84,6 +92,13 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
           const int e = tid + it * JT;
           if (e < 2 * JBLK * bw) { sW[e] = lw[it]; sJ[e] = lj[it]; }
         }
+      }
+      // the round's rotations are accumulated in the 32 x 32 sQ (= I here) and applied to the
+      // staged J columns once, at the end of the round (J_blk := J_blk sQ), instead of rotating the
+      // b-row J columns at every step: half the shared-memory traffic of the inner sweep
+      for (int e = tid; e < 2 * JBLK * 2 * JBLK; e += JT) {
+        const int c = e / (2 * JBLK), r = e % (2 * JBLK);
+        sQ[c * (2 * JBLK + 1) + r] = r == c ? 1.0 : 0.0;
       }
       __syncthreads();
       // squared column norms, recomputed from the data once per round and then updated exactly
@@ -129,25 +144,19 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
               const double t = (d >= 0.0 ? 2.0 * gm : -2.0 * gm) / (fabs(d) + sqrt(d * d + 4.0 * gm * gm));
               const double cs = rsqrt(1.0 + t * t);
               const double sn = cs * t;
-              double* ji = sJ + a * bw;
-              double* jj = sJ + b * bw;
-              double u[RPL], v[RPL];
-#pragma unroll
-              for (int k = 0; k < RPL; ++k) {
-                const int row = lane + 32 * k;
-                u[k] = row < bw ? ji[row] : 0.0;
-                v[k] = row < bw ? jj[row] : 0.0;
-              }
+              double* qi = sQ + a * (2 * JBLK + 1);
+              double* qj = sQ + b * (2 * JBLK + 1);
+              const double u = qi[lane], v = qj[lane];     // 2 JBLK == 32 rows: one per lane
 #pragma unroll
               for (int k = 0; k < RPL; ++k) {
                 const int row = lane + 32 * k;
                 if (row < bw) {
                   wi[row] = cs * x[k] - sn * y[k];
                   wj[row] = sn * x[k] + cs * y[k];
-                  ji[row] = cs * u[k] - sn * v[k];
-                  jj[row] = sn * u[k] + cs * v[k];
                 }
               }
+              qi[lane] = cs * u - sn * v;
+              qj[lane] = sn * u + cs * v;
               __syncwarp();                                  // every lane has read s_nrm[a], s_nrm[b]
               if (lane == 0) {
                 s_nrm[a] = fmax(al - t * gm, 0.0);
@@ -163,22 +172,41 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
       if (c == 0 && tid == 0 && trk < 32) g_jac_trace[trk * 8 + 2] = clock64();
 #endif
       {
-        double lw[PER], lj[PER];
+        // J_blk := J_blk sQ (bw x 32 x 32) on the FP64 tensor cores: warp w owns rows 16w..16w+15,
+        // all four 8-column tiles; the result goes straight to global memory
+        const int g = lane >> 2, t4 = lane & 3;
+        if (16 * warp < bw) {
+          double d[4][4] = {};
+#pragma unroll
+          for (int ks = 0; ks < 2 * JBLK / 4; ++ks) {
+            const int k0 = 4 * ks + t4;
+            const int ra = 16 * warp + g, rb = ra + 8;
+            const double a0 = ra < bw ? sJ[k0 * bw + ra] : 0.0;
+            const double a1 = rb < bw ? sJ[k0 * bw + rb] : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) dmma16884(d[nt], a0, a1, sQ[(8 * nt + g) * (2 * JBLK + 1) + k0]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int row = 16 * warp + g + ((q & 2) ? 8 : 0), col = 8 * nt + 2 * t4 + (q & 1);
+              const int gc = s_gcol[col];
+              if (row < bw && gc < bw) __stcg(J + (size_t)gc * bw + row, d[nt][q]);
+            }
+        }
+        double lw[PER];
 #pragma unroll
         for (int it = 0; it < PER; ++it) {
           const int e = tid + it * JT;
           lw[it] = e < 2 * JBLK * bw ? sW[e] : 0.0;
-          lj[it] = e < 2 * JBLK * bw ? sJ[e] : 0.0;
         }
 #pragma unroll
         for (int it = 0; it < PER; ++it) {
           const int e = tid + it * JT;
           if (e < 2 * JBLK * bw) {
             const int col = e / bw, row = e % bw, gc = s_gcol[col];
-            if (gc < bw) {
-              __stcg(W + (size_t)gc * bw + row, lw[it]);
-              __stcg(J + (size_t)gc * bw + row, lj[it]);
-            }
+            if (gc < bw) __stcg(W + (size_t)gc * bw + row, lw[it]);
           }
         }
       }

@@ -20,11 +20,14 @@ for m, w in ((50000, 256), (20000, 256), (2000, 256), (256, 256), (50000, 32)):
         P.copy_(P0); h.hqr(P)
     res[f"hqr_{m}x{w}_ms"] = timeit(f)
     print(f"hqr {m}x{w}", res[f"hqr_{m}x{w}_ms"], "ms", flush=True)
+torch.manual_seed(5)
 R = torch.triu(torch.randn(256, 256, dtype=torch.float64, device="cuda")).t().contiguous().t()
 def g():
     h.svd_small(R)
 res["svd_small_256_ms"] = timeit(g)
-print("svd_small 256", res["svd_small_256_ms"], "sweeps", h.svd_small(R)[3], flush=True)
+sw = h.svd_small(R)[3]
+res["svd_small_256_sweeps"] = sw
+print("svd_small 256", res["svd_small_256_ms"], "ms, sweeps", sw, "->", res["svd_small_256_ms"] / sw, "ms per sweep", flush=True)
 json.dump(res, open("gpurun_out/panel_bench.json", "w"), indent=1)
 if len(sys.argv) > 1:   # profiling mode: one more call of each
     P.copy_(P0); h.hqr(P); h.svd_small(R); torch.cuda.synchronize()
