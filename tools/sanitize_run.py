@@ -94,8 +94,43 @@ def case_ooc():
     check(X, X0, "out-of-core 400x352")
 
 
+def case_dist_ooc():
+    """multi-GPU x out-of-core: an in-process group of 2 ranks streaming their host shards"""
+    import threading
+    from paper_2408_05238_b200 import dist as D
+    os.environ["UTV_OOC_MAX_RESIDENT_COLS"] = "0"
+    m, n, r, b = 400, 352, 150, 64
+    G = gen.GpMatrix(m, n, r, seed=3)
+    B, X0 = G.known_rhs(k=2)
+    Ad = dev(G.A)
+    hs = utv.local_group(2)
+    shards = []
+    for p in range(2):
+        sh = D.scatter_columns(Ad, b, 2, p)
+        t = utv.colmajor_empty(m, sh.shape[1], device="cpu", pin_memory=True)
+        t.copy_(sh)
+        shards.append(t)
+    Bs = [dev(B) for _ in range(2)]
+    Xs = [utv.colmajor_empty(n, 2) for _ in range(2)]
+    out = [None, None]
+
+    def work(p):
+        out[p] = hs[p].lstsq(shards[p], Bs[p], Xs[p], utv.Opts(block=b, power_iters=1, tau=1e-10, seed=1,
+                                                               flags=utv.UTV_HOST_STREAMED))
+    ts = [threading.Thread(target=work, args=(p,)) for p in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    assert out == [150, 150], out
+    check(Xs[0], X0, "dist streamed 400x352 P=2")
+    for h in hs:
+        h.close()
+
+
 CASES = {"lstsq": case_lstsq, "lstsq256": case_lstsq_b256, "qrglobal": case_qr_global, "gemm": case_gemm_cfgs,
-         "wide": case_wide, "ooc": case_ooc}
+         "wide": case_wide, "ooc": case_ooc, "distooc": case_dist_ooc}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
