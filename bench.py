@@ -465,6 +465,10 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     prof = h.profile_read()
+    try:
+        jac_failed, jac_sweeps = h.svd_status()       # Jacobi sweeps: max over the blocks of the last call
+    except Exception:                                  # noqa: BLE001 -- diagnostics only
+        jac_failed, jac_sweeps = None, None
     dump = args.profile_dump or os.path.join("/tmp", f"utv_prof_{os.getpid()}.csv")
     h.profile_dump(dump)
     big = big_gemm_stats(dump)
@@ -578,6 +582,7 @@ def run_ours(args):
         "phases_note": "sums of event-bracketed launch times per kernel family over all streams; the SVD "
                        "runs on a low-priority side stream overlapping the main stream, so its times include "
                        "waiting for SMs (profiles/r01_timeline_cfg3_summary.txt has the critical path)",
+        "jacobi_max_sweeps": jac_sweeps,
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk,
