@@ -72,8 +72,11 @@ utv_status utv_create(utv_handle* handle, int device, void* stream);
  * U^T B; X (n x k, device) is written, identical on every rank; *rank is identical on every rank.
  * All ranks must make the same calls with the same m, n, k, opts (collectives in lock step).
  * Fast option with factored V only (UTV_NULLIFY_T12 / UTV_EXPLICIT_V -> UTV_ERR_UNSUPPORTED);
- * utv_factor on such a handle -> UTV_ERR_UNSUPPORTED.  With UTV_HOST_STREAMED the shard A is in
- * HOST memory (pinned, or registered for the call) and is streamed through the rank's device
+ * utv_factor on such a handle: A = the rank's shard (-> its shard of T), V (if non-NULL) = the rank's
+ * CONTIGUOUS row block of V, rows [p ceil(n/P), min(n, (p+1) ceil(n/P))) x n columns (device,
+ * ldv >= its row count), B replicated -> U^T B; U (UTV_WANT_U), UTV_NULLIFY_T12 and
+ * UTV_HOST_STREAMED -> UTV_ERR_UNSUPPORTED.  In utv_lstsq, with UTV_HOST_STREAMED the shard A is
+ * in HOST memory (pinned, or registered for the call) and is streamed through the rank's device
  * (out-of-core x multi-GPU, SURVEY 8(e) x 8(f) #1; the device budget is per handle); B, X stay on
  * the device.
  * Failures: the ranks first agree on the call (one AllReduce of a flag after every rank has checked

@@ -212,11 +212,20 @@ class Handle:
         self.check(lib().utv_synchronize(self.h))
 
     # ------------------------------------------------------------------ the boundary calls
-    def factor(self, A, V=None, U=None, B=None, opts: Opts | None = None, want_rank: bool = True):
-        """randUTV in place: A -> T; V, U (if given; U needs opts.flags & UTV_WANT_U), B -> U^T B."""
+    def factor(self, A, V=None, U=None, B=None, opts: Opts | None = None, want_rank: bool = True,
+               n: int | None = None):
+        """randUTV in place: A -> T; V, U (if given; U needs opts.flags & UTV_WANT_U), B -> U^T B.
+        On a multi-GPU handle A is this rank's block-cyclic shard, V (optional) this rank's row block
+        of V (ceil(n/P) x n) and n the GLOBAL column count (default V.shape[1])."""
         opts = opts or Opts()
         _check_f64(A, V, U, B)
-        m, n = A.shape
+        m, n_a = A.shape
+        if getattr(self, "multi", False):
+            n = n if n is not None else (V.shape[1] if V is not None else None)
+            if n is None:
+                raise ValueError("multi-GPU factor: pass the global n (or V)")
+        else:
+            n = n_a
         k = 0 if B is None else (B.shape[1] if B.dim() == 2 else 1)
         r = C.c_int64(-1)
         o = opts.c()

@@ -1377,8 +1377,40 @@ void dist_solve_z(const Ctx& c, Comm& comm, int64_t r, int64_t b, const double* 
   }
 }
 
+// V's row block [v0, v0 + nrows) (nrows x n, ldv) from the factored V = Q_1 ... Q_s D (every rank
+// holds the same factors): E^T V with the right multiplications applied in order, Q_1 first.
+void factored_v_rows(const Ctx& c, const FactoredV& fv, int64_t n, int64_t b, int64_t v0, int64_t nrows, double* V,
+                     int64_t ldv) {
+  cudaStream_t st = c.st;
+  if (nrows <= 0) return;
+  launch_set_zero(st, nrows, n, V, ldv);
+  launch_set_identity(st, nrows, nrows, V + cm(0, v0, ldv), ldv);
+  double *t1 = c.at(c.L.X), *t2 = c.at(c.L.X2);
+  for (size_t i = 0; i < fv.woff.size(); ++i) {                             // X := X Q_i
+    const int64_t j0 = fv.j0[i], np = fv.np[i];
+    const double* W = fv.W + fv.woff[i];
+    double* Xc = V + cm(0, j0, ldv);
+    c.gemm(false, false, nrows, b, np, 1.0, Xc, ldv, W, np, 0.0, t1, nrows);
+    c.gemm(false, false, nrows, b, b, 1.0, t1, nrows, fv.T + (size_t)(j0 / b) * b * b, b, 0.0, t2, nrows);
+    c.gemm(false, true, nrows, np, b, -1.0, t2, nrows, W, np, 1.0, Xc, ldv);
+  }
+  for (int64_t j0 = 0, step = 0; j0 < n; j0 += b, ++step) {                 // X := X D
+    const int64_t bw = std::min(b, n - j0);
+    c.gemm(false, false, nrows, bw, bw, 1.0, V + cm(0, j0, ldv), ldv, fv.Vs + (size_t)step * b * b, b, 0.0, t1, nrows);
+    launch_copy(st, nrows, bw, t1, nrows, V + cm(0, j0, ldv), ldv);
+  }
+}
+
+// Rows of V held by rank p (contiguous row blocks of ceil(n / P)).
+void dist_v_rows(int64_t n, int P, int p, int64_t* v0, int64_t* nrows) {
+  const int64_t per = (n + P - 1) / P;
+  *v0 = std::min<int64_t>(n, (int64_t)p * per);
+  *nrows = std::min<int64_t>(n, *v0 + per) - *v0;
+}
+
 int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int64_t lda, double* B, int64_t ldb,
-                   double* X, int64_t ldx, const utv_opts& opt) {
+                   double* X, int64_t ldx, const utv_opts& opt, bool solve = true, double* Vrows = nullptr,
+                   int64_t ldv = 0) {
   Comm& comm = *h->comm;
   const int P = comm.nranks, p = comm.rank;
   const int64_t b = opt.block, nb = (n + b - 1) / b;
@@ -1586,6 +1618,15 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   if (flo[1] != 0.0) fail(UTV_ERR_NUMERICAL, "Jacobi SVD of a diagonal block did not converge in 30 sweeps");
   const int64_t r = finish_factor(c, n, dg, 0, opt.tau, true);                          // a8 (replicated)
   if (kp) { kp->r = r; kp->valid = true; }
+  if (!solve) {                                                                          // utv_factor
+    if (Vrows) {
+      int64_t v0, nv;
+      dist_v_rows(n, P, p, &v0, &nv);
+      factored_v_rows(c, fv, n, b, v0, nv, Vrows, ldv);
+    }
+    comm.wait(st);
+    return r;
+  }
   if (k <= 0) return r;
   dist_solve_z(c, comm, r, b, A, lda, B, ldb, k);                                        // a9
   solve_factored(c, n, r, nullptr, 0, nullptr, 0, k, X, ldx, fv, b, nullptr, true);      // X = V z (replicated)
@@ -2077,8 +2118,40 @@ utv_status utv_synchronize(utv_handle h) {
 utv_status utv_factor(utv_handle h, int64_t m, int64_t n, double* A, int64_t lda, double* V, int64_t ldv, double* U,
                       int64_t ldu, double* B, int64_t ldb, int64_t k, const utv_opts* opts, int64_t* rank) {
   return guarded(h, [&] {
+    if (h->comm) {                                                     // multi-GPU handle
+      // A = this rank's block-cyclic shard -> its shard of T; V (if non-NULL) = this rank's
+      // contiguous row block of V (ceil(n/P) rows, ldv >= them); B replicated -> U^T B.  The ranks
+      // agree on the call before the first collective, as in utv_lstsq.
+      utv_status local = UTV_OK;
+      std::string msg;
+      try {
+        check_opts(opts);
+        if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
+        if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
+        if ((U && (opts->flags & UTV_WANT_U)) || (opts->flags & (UTV_NULLIFY_T12 | UTV_HOST_STREAMED)))
+          fail(UTV_ERR_UNSUPPORTED, "multi-GPU utv_factor: no U, no UTV_NULLIFY_T12, no UTV_HOST_STREAMED");
+        check_ld("lda", lda, m);
+        int64_t v0 = 0, nv = 0;
+        if (n > 0) dist_v_rows(n, h->comm->nranks, h->comm->rank, &v0, &nv);
+        if (V) check_ld("ldv", ldv, nv);
+        if (B && k > 0) check_ld("ldb", ldb, m);
+        const int64_t nloc = n > 0 ? dist_local_cols(n, opts->block, h->comm->nranks, h->comm->rank) : 0;
+        if (nloc > 0 && !A) fail(UTV_ERR_ARG, "A is NULL");
+        if ((nloc > 0 && !is_device_ptr(A)) || (V && !is_device_ptr(V)) || (B && k > 0 && !is_device_ptr(B)))
+          fail(UTV_ERR_ARG, "the multi-GPU path takes device pointers");
+        if (n > 0) dist_reserve(h, m, n, k, *opts);
+      } catch (const ApiError& e) {
+        local = e.st;
+        msg = e.msg;
+      }
+      dist_agree(h, local, msg);
+      if (n == 0) { if (rank) *rank = 0; return; }
+      const int64_t r = lstsq_dist(h, m, n, (B && k > 0) ? k : 0, A, lda, B, ldb, nullptr, 1, *opts, false, V,
+                                   ldv);
+      if (rank) *rank = r;
+      return;
+    }
     check_opts(opts);
-    if (h->comm) fail(UTV_ERR_UNSUPPORTED, "a multi-GPU handle implements utv_lstsq only");
     if (m < 0 || n < 0 || k < 0) fail(UTV_ERR_ARG, "negative dimension");
     if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
     if (n > 0 && !A) fail(UTV_ERR_ARG, "A is NULL");

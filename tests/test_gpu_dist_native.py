@@ -126,13 +126,14 @@ def test_nccl_single_rank(utv):
     assert np.linalg.norm(Xs[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)
 
 
-def test_dist_handle_rejects_factor_and_flags(utv):
+def test_dist_handle_rejects_unsupported_flags(utv):
     hs = utv.local_group(1)
     h = hs[0]
     try:
         A = utv.colmajor_empty(64, 64).zero_()
+        U = utv.colmajor_empty(64, 64)
         with pytest.raises(utv.UtvError) as e:
-            h.factor(A)
+            h.factor(A, U=U, opts=utv.Opts(block=16, flags=utv.UTV_WANT_U), n=64)
         assert e.value.status == utv.UTV_ERR_UNSUPPORTED
         B = utv.colmajor_empty(64, 1).zero_()
         X = utv.colmajor_empty(64, 1)
@@ -249,3 +250,61 @@ def test_local_group_chunks_and_svd_lag(utv, P, chunks, lag):
         assert np.linalg.norm(Xs[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)
         res[lg] = Xs[0]
     assert np.linalg.norm(res[1] - res[lag]) <= 1e-12 * np.linalg.norm(res[1])
+
+
+@pytest.mark.parametrize("P,m,n,r,b,q,k", [(2, 600, 520, 250, 64, 1, 2), (3, 700, 700, 300, 64, 2, 1),
+                                          (1, 500, 400, 180, 64, 1, 1)])
+def test_local_group_factor(utv, P, m, n, r, b, q, k):
+    """utv_factor on a multi-GPU handle (SURVEY 8(b) distributed mode): every rank's shard of T,
+    its contiguous row block of V and the replicated C = U^T B.  Gathered, they satisfy: V orthogonal,
+    ||(A V)_j|| = ||T_j|| per column (A V = U T), T zero below the diagonal, and x = V(:, 0:r)
+    T11^{-1} C(0:r) equal to the oracle's least-squares solution (1e-9); rank identical."""
+    M = gen.GpMatrix(m, n, r, seed=m + n + 7 * P)
+    B, _ = M.known_rhs(k=k)
+    B = B.reshape(m, -1)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=6)
+    Ad = dev(M.A)
+    hs = utv.local_group(P)
+    per = (n + P - 1) // P
+    try:
+        shards = [utv.colmajor(D.scatter_columns(Ad, b, P, p).clone()) for p in range(P)]
+        Bs = [dev(B) for _ in range(P)]
+        Vs = [utv.colmajor_empty(max(1, min(n, (p + 1) * per) - min(n, p * per)), n) for p in range(P)]
+        torch.cuda.synchronize()
+        out, err = [None] * P, [None] * P
+
+        def work(p):
+            try:
+                Ap = shards[p] if shards[p].shape[1] > 0 else utv.colmajor_empty(m, 1)
+                out[p] = hs[p].factor(Ap, V=Vs[p], B=Bs[p], opts=utv.Opts(block=b, power_iters=q, tau=1e-10, seed=6),
+                                      n=n)
+            except Exception as e:          # noqa: BLE001
+                err[p] = e
+
+        ts = [threading.Thread(target=work, args=(p,)) for p in range(P)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=600)
+        assert not any(t.is_alive() for t in ts), "a rank hung"
+        for e in err:
+            if e is not None:
+                raise e
+        torch.cuda.synchronize()
+        T = D.gather_columns(shards, n, b).cpu().numpy()
+        V = np.vstack([Vs[p][:min(n, (p + 1) * per) - min(n, p * per)].cpu().numpy() for p in range(P)])
+        C = Bs[0].cpu().numpy()
+        for Bp in Bs[1:]:
+            assert np.array_equal(Bp.cpu().numpy(), C)                  # replicated U^T B
+    finally:
+        for h in hs:
+            h.close()
+    assert out == [ro] * P and ro == r, (out, ro)
+    assert np.abs(V.T @ V - np.eye(n)).max() <= 1e-13
+    assert np.all(np.tril(T, -1) == 0.0)
+    AV = M.A @ V
+    nrm_av, nrm_t = np.linalg.norm(AV, axis=0), np.linalg.norm(T, axis=0)
+    assert np.abs(nrm_av - nrm_t).max() <= 1e-12 * np.linalg.norm(M.A)
+    z = np.linalg.solve(T[:r, :r], C[:r])
+    X = V[:, :r] @ z
+    assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
