@@ -75,7 +75,9 @@ utv_status utv_create(utv_handle* handle, int device, void* stream);
  * utv_factor on such a handle: A = the rank's shard (-> its shard of T), V (if non-NULL) = the rank's
  * CONTIGUOUS row block of V, rows [p ceil(n/P), min(n, (p+1) ceil(n/P))) x n columns (device,
  * ldv >= its row count), B replicated -> U^T B; U (UTV_WANT_U), UTV_NULLIFY_T12 and
- * UTV_HOST_STREAMED -> UTV_ERR_UNSUPPORTED.  In utv_lstsq, with UTV_HOST_STREAMED the shard A is
+ * UTV_HOST_STREAMED -> UTV_ERR_UNSUPPORTED.  utv_solve on such a handle: T = the rank's shard of T
+ * (block-cyclic with the block size of the handle's last utv_factor / utv_lstsq), V = its row block,
+ * C replicated; X (n x k) is written, identical on every rank.  In utv_lstsq, with UTV_HOST_STREAMED the shard A is
  * in HOST memory (pinned, or registered for the call) and is streamed through the rank's device
  * (out-of-core x multi-GPU, SURVEY 8(e) x 8(f) #1; the device budget is per handle); B, X stay on
  * the device.

@@ -235,8 +235,12 @@ class Handle:
         return int(r.value) if want_rank else None
 
     def solve(self, T, V, Cm, r: int, X):
+        """X = V(:, 0:r) T11^{-1} C(0:r).  On a multi-GPU handle T is this rank's shard, V its row
+        block and the global n is X.shape[0]."""
         _check_f64(T, V, Cm, X)
         m, n = T.shape
+        if getattr(self, "multi", False):
+            n = X.shape[0]
         k = Cm.shape[1] if Cm.dim() == 2 else 1
         self.check(lib().utv_solve(self.h, m, n, int(r), _ptr(T), _ld(T), _ptr(V), _ld(V), _ptr(Cm), _ld(Cm), k,
                                    _ptr(X), _ld(X)))

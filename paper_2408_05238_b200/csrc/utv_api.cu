@@ -329,6 +329,7 @@ struct utv_handle_s {
   int coop_share = 1;            // ranks of an in-process group sharing this device (cooperative-CTA cap)
   double* dbuf = nullptr; size_t dbuf_doubles = 0;
   Kept kept;                     // UTV_KEEP_FACTORS
+  int64_t dist_block = 0;        // multi-GPU: block size of the last utv_factor / utv_lstsq (T's layout)
   Profiler prof;
 };
 
@@ -1416,6 +1417,7 @@ int64_t lstsq_dist(utv_handle h, int64_t m, int64_t n, int64_t k, double* A, int
   const int64_t b = opt.block, nb = (n + b - 1) / b;
   const int64_t nloc = dist_local_cols(n, b, P, p);
   cudaStream_t st = h->stream, cs = h->cst;
+  h->dist_block = b;
   const int ns = h->num_sms;
   Ctx c = make_ctx(h, m, n, k, b);
   const Layout& L = c.L;
@@ -1731,6 +1733,7 @@ int64_t lstsq_dist_ooc(utv_handle h, Ooc& o, int64_t m, int64_t n, int64_t k, do
   const int P = comm.nranks, p = comm.rank;
   const int64_t b = opt.block, nb = (n + b - 1) / b, nloc = o.n;
   cudaStream_t st = h->stream;
+  h->dist_block = b;
   const int ns = h->num_sms;
   Ctx c = make_ctx(h, m, n, k, b);
   const Layout& L = c.L;
@@ -2179,6 +2182,56 @@ utv_status utv_factor(utv_handle h, int64_t m, int64_t n, double* A, int64_t lda
 utv_status utv_solve(utv_handle h, int64_t m, int64_t n, int64_t r, const double* T, int64_t ldt, const double* V,
                      int64_t ldv, const double* C, int64_t ldc, int64_t k, double* X, int64_t ldx) {
   return guarded(h, [&] {
+    if (h->comm) {
+      // multi-GPU handle: T = this rank's block-cyclic shard (block size of the handle's last
+      // utv_factor / utv_lstsq), V = its contiguous row block, C replicated; z = T11^{-1} C(0:r) by
+      // the distributed block back substitution, X's row block = V_p(:, 0:r) z, AllGather(X rows).
+      Comm& comm = *h->comm;
+      const int P = comm.nranks, p = comm.rank;
+      utv_status local = UTV_OK;
+      std::string msg;
+      int64_t v0 = 0, nv = 0, per = 0;
+      const int64_t b = h->dist_block;
+      try {
+        if (m < 0 || n < 0 || k < 0 || r < 0 || r > n) fail(UTV_ERR_ARG, "bad dimension (need 0 <= r <= n)");
+        if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
+        if (b < 1) fail(UTV_ERR_ARG, "multi-GPU utv_solve needs a preceding utv_factor on this handle");
+        dist_v_rows(n, P, p, &v0, &nv);
+        per = (n + P - 1) / P;
+        check_ld("ldt", ldt, m); check_ld("ldv", ldv, nv); check_ld("ldc", ldc, m); check_ld("ldx", ldx, n);
+        if (k > 0 && n > 0 && (!X || (r > 0 && (!C || (nv > 0 && !V)) ||
+                                     (r > 0 && dist_local_cols(r, b, P, p) > 0 && !T))))
+          fail(UTV_ERR_ARG, "NULL matrix");
+        if (k > 0 && n > 0) {
+          make_ctx(h, m, n, k, b);
+          ensure_buf(&h->dbuf, &h->dbuf_doubles, std::max(dist_dbuf_doubles(n, b, P, k), (size_t)(P + 1) * per * k));
+        }
+      } catch (const ApiError& e) {
+        local = e.st;
+        msg = e.msg;
+      }
+      dist_agree(h, local, msg);
+      if (k == 0 || n == 0) return;
+      Ctx c = make_ctx(h, m, n, k, b);
+      cudaStream_t st = h->stream;
+      double* Zb = c.at(c.L.zsolve);
+      launch_set_zero(st, n, k, X, ldx);
+      if (r > 0) {
+        dist_solve_z(c, comm, r, b, T, ldt, C, ldc, k);                   // z = T11^{-1} C(0:r) (ld r)
+        double* mine = h->dbuf;                                            // per x k, this rank's rows
+        double* all = mine + (size_t)per * k;                              // P x (per x k)
+        launch_set_zero(st, per, k, mine, per);
+        if (nv > 0) c.gemm(false, false, nv, k, r, 1.0, V, ldv, Zb, r, 0.0, mine, per);
+        comm.allgather(mine, all, (size_t)per * k, st);
+        for (int q = 0; q < P; ++q) {
+          int64_t q0, qn;
+          dist_v_rows(n, P, q, &q0, &qn);
+          if (qn > 0) launch_copy(st, qn, k, all + (size_t)q * per * k, per, X + q0, ldx);
+        }
+      }
+      comm.wait(st);
+      return;
+    }
     if (m < 0 || n < 0 || k < 0 || r < 0 || r > n) fail(UTV_ERR_ARG, "bad dimension (need 0 <= r <= n)");
     if (m < n) fail(UTV_ERR_SHAPE, "m < n is not supported (R4)");
     check_ld("ldt", ldt, m); check_ld("ldv", ldv, n); check_ld("ldc", ldc, m); check_ld("ldx", ldx, n);

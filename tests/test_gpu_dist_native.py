@@ -308,3 +308,50 @@ def test_local_group_factor(utv, P, m, n, r, b, q, k):
     z = np.linalg.solve(T[:r, :r], C[:r])
     X = V[:, :r] @ z
     assert np.linalg.norm(X - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
+def test_local_group_factor_then_solve(utv):
+    """utv_factor then utv_solve on a multi-GPU handle: the distributed block back substitution on
+    the T shards, X's row blocks from the V row blocks, AllGather -- X replicated, equal on every
+    rank and to the oracle's solution."""
+    P, m, n, r, b, q = 3, 650, 600, 270, 64, 1
+    M = gen.GpMatrix(m, n, r, seed=99)
+    B, _ = M.known_rhs(k=2)
+    Xo, ro = oracle.lstsq(M.A, B, b=b, q=q, tau=1e-10, seed=2)
+    Ad = dev(M.A)
+    hs = utv.local_group(P)
+    per = (n + P - 1) // P
+    try:
+        shards = [utv.colmajor(D.scatter_columns(Ad, b, P, p).clone()) for p in range(P)]
+        Bs = [dev(B) for _ in range(P)]
+        Vs = [utv.colmajor_empty(max(1, min(n, (p + 1) * per) - min(n, p * per)), n) for p in range(P)]
+        Xs = [utv.colmajor_empty(n, 2) for _ in range(P)]
+        rk = [None] * P
+        err = [None] * P
+
+        def work(p):
+            try:
+                rk[p] = hs[p].factor(shards[p], V=Vs[p], B=Bs[p], opts=utv.Opts(block=b, power_iters=q, tau=1e-10,
+                                                                                    seed=2), n=n)
+                hs[p].solve(shards[p], Vs[p], Bs[p], rk[p], Xs[p])
+            except Exception as e:          # noqa: BLE001
+                err[p] = e
+
+        ts = [threading.Thread(target=work, args=(p,)) for p in range(P)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=600)
+        assert not any(t.is_alive() for t in ts), "a rank hung"
+        for e in err:
+            if e is not None:
+                raise e
+        torch.cuda.synchronize()
+        X = [x.cpu().numpy() for x in Xs]
+    finally:
+        for h in hs:
+            h.close()
+    assert rk == [ro] * P and ro == r
+    for x in X:
+        assert np.array_equal(x, X[0])
+    assert np.linalg.norm(X[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)
