@@ -86,15 +86,33 @@ def check_hqr(P, Pd, W, tau, T):
 
 # ---------------------------------------------------------------------------- a3 / a5 at full height
 @pytest.mark.parametrize("m,w", [(110000, 32), (120000, 64), (120000, 256)])
-def test_hqr_full_height_global_variant(utv, h, tmp_path, m, w):
-    """m > 101 376: the automatic choice is the global-memory kernel (as for every cfg4 panel)."""
+@pytest.mark.parametrize("variant", ["hybrid", "global"])
+def test_hqr_full_height(utv, h, tmp_path, m, w, variant):
+    """m > 101 376 (rows per CTA > 768, as in every cfg4 panel): automatically the hybrid kernel
+    (each CTA's first 768 rows in shared memory, the rest re-read from L2 per column, tag 3);
+    forced, the global-memory kernel (tag 0)."""
     rng = np.random.default_rng(m + w)
     P = rng.standard_normal((m, w))
-    h.profile(True)
-    Pd, W, tau, T = h.hqr(dev(P))
-    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
-    assert recs and all(r["tag"] == 0 for r in recs)                              # global variant only
+    with utv.tuned(utv.UTV_TUNE_QR_GLOBAL, 1 if variant == "global" else 0):
+        h.profile(True)
+        Pd, W, tau, T = h.hqr(dev(P))
+        recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    assert recs and all(r["tag"] == (0 if variant == "global" else 3) for r in recs)
     assert max(r["K"] for r in recs) > 100                                        # cooperative grid
+    check_hqr(P, Pd, W, tau, T)
+
+
+@pytest.mark.parametrize("m,w,ctas", [(9000, 64, 7), (9000, 256, 5), (3001, 200, 2), (2000, 33, 2)])
+def test_hqr_hybrid_small(utv, h, tmp_path, m, w, ctas):
+    """The hybrid kernel at sizes the oracle factors quickly: a CTA cap leaves more than 768 rows
+    per CTA (shared-memory head + global tail, ragged widths and sub-panels)."""
+    rng = np.random.default_rng(11 * m + w + ctas)
+    P = rng.standard_normal((m, w))
+    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas):
+        h.profile(True)
+        Pd, W, tau, T = h.hqr(dev(P))
+        recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    assert recs and all(r["tag"] == 3 for r in recs)
     check_hqr(P, Pd, W, tau, T)
 
 
@@ -179,18 +197,21 @@ def test_lstsq_n3072_b256_q2_long_k_tiles(utv, h, tmp_path):
     assert any(((r["tag"] >> 2) & 63) == 0 and (r["tag"] & 1) == 1 for r in long_k)     # TN: Y = A'^T Z
 
 
-def test_lstsq_tall_global_panels(utv, h, tmp_path):
+@pytest.mark.parametrize("variant", ["hybrid", "global"])
+def test_lstsq_tall_panels(utv, h, tmp_path, variant):
     """cfg4's shape family (tall, 16 RHS, q = 1) at m = 120 000 x n = 512: every a5 panel has more
-    than 101 376 rows, so the panel QR runs the global-memory kernel inside the solver."""
+    than 101 376 rows -- the hybrid kernel (automatic) or the global-memory one (forced) inside
+    the solver."""
     M = gen.GpMatrix(120000, 512, 384, seed=32)
     B, X0 = M.known_rhs(k=16)
     Xo, ro = oracle.lstsq(M.A, B, b=256, q=1, tau=1e-10, seed=gen.SKETCH_SEED)
-    Xg, rg, recs = _lstsq_profiled(utv, h, tmp_path, M.A, B, 256, 1, gen.SKETCH_SEED)
+    with utv.tuned(utv.UTV_TUNE_QR_GLOBAL, 1 if variant == "global" else 0):
+        Xg, rg, recs = _lstsq_profiled(utv, h, tmp_path, M.A, B, 256, 1, gen.SKETCH_SEED)
     assert rg == ro == 384
     assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
     assert np.linalg.norm(Xg - X0) <= 1e-10 * np.linalg.norm(X0)
     panels = [r for r in recs if r["family"] == 1 and r["M"] > 101376]
-    assert panels and all(r["tag"] == 0 for r in panels)
+    assert panels and all(r["tag"] == (0 if variant == "global" else 3) for r in panels)
 
 
 @pytest.mark.parametrize("cfg", [0, 2, 3])
@@ -205,3 +226,4 @@ def test_lstsq_forced_tile_config(utv, h, tmp_path, cfg):
     assert rg == ro == 450
     assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
     assert {c for c, _ in gemm_cfgs(recs)} == {cfg}
+
