@@ -75,14 +75,14 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[NBMAX], int nb,
 // zeros below R written at the end.  CTA c owns rows [c L, (c+1) L); SMEM: those rows live in
 // shared memory for the whole kernel, else each row is re-read from global (L2) per column with
 // all its loads in flight.  One grid barrier per column.
-template <bool SMEM, bool HYB = false>
+template <bool SMEM, bool HYB = false, int SR = SROW>
 __global__ void __launch_bounds__(QR_THREADS, 1)
 qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __restrict__ W, int64_t ldw, int64_t wtop,
            double* __restrict__ tau, double* __restrict__ T, int64_t ldt, double* __restrict__ part,
            unsigned* __restrict__ bar, int64_t Ls) {
   // SMEM: the first Ls rows of each CTA's range live in shared memory for the whole kernel, the
   // rest (tall panels: hybrid) are re-read from global memory / L2 per column; !SMEM: Ls = 0.
-  extern __shared__ double sp[];             // [Ls][SROW] (SMEM only)
+  extern __shared__ double sp[];             // [Ls][SR] (SMEM only)
   __shared__ double red_w[(QR_THREADS / 32) * NBMAX];
   __shared__ double red[NBMAX];
   __shared__ double piv[NBMAX];              // row j: W values (< j) and P values (>= j)
@@ -110,7 +110,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   if constexpr (SMEM) {
     for (int64_t e = tid; e < (rs - r0) * nb; e += QR_THREADS) {
       const int64_t il = e % (rs - r0), c = e / (rs - r0);
-      sp[il * SROW + c] = P[cm(r0 + il, c, ldp)];
+      sp[il * SR + c] = P[cm(r0 + il, c, ldp)];
     }
   }
   __syncthreads();
@@ -123,10 +123,10 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   for (int64_t i = r0 + tid; i < r1; i += QR_THREADS) {        // column 0: rows i > 0
     if (i < 1) continue;
     const bool sm = in_smem(i);
-    const double x0 = sm ? sp[(i - r0) * SROW] : P[cm(i, 0, ldp)];
+    const double x0 = sm ? sp[(i - r0) * SR] : P[cm(i, 0, ldp)];
 #pragma unroll
     for (int p = 0; p < NBMAX; ++p)
-      if (p < nb) acc[p] += x0 * (sm ? sp[(i - r0) * SROW + p] : P[cm(i, p, ldp)]);
+      if (p < nb) acc[p] += x0 * (sm ? sp[(i - r0) * SR + p] : P[cm(i, p, ldp)]);
   }
 
   // part: double-buffered by column parity; slot (buf, c) = CTA c's partial sums at [0, nb) and,
@@ -163,13 +163,13 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
     const unsigned owner = (unsigned)(j / L);
     if (G == 1) {
       block_reduce_store<false>(acc, nb, red_w, red, 1);
-      if (tid < nb) piv[tid] = in_smem(j) ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)];
+      if (tid < nb) piv[tid] = in_smem(j) ? sp[(j - r0) * SR + tid] : P[cm(j, tid, ldp)];
       t_column(j - 1, tj_prev);
       __syncthreads();
     } else {
       block_reduce_store<true>(acc, nb, red_w, pelem(buf, 0, blockIdx.x), (int)G);
       if (blockIdx.x == owner && tid < nb)
-        __stcg(pelem(buf, NBMAX + tid, owner), in_smem(j) ? sp[(j - r0) * SROW + tid] : P[cm(j, tid, ldp)]);
+        __stcg(pelem(buf, NBMAX + tid, owner), in_smem(j) ? sp[(j - r0) * SR + tid] : P[cm(j, tid, ldp)]);
       tr(j, 3);
 #ifdef UTV_QR_TRACE
       if (j == 5 && tid == 0 && blockIdx.x < 256) g_qr_arrive[blockIdx.x] = gtimer();
@@ -240,7 +240,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
       // column j keeps its pre-scaling value in registers, so acc[j] is rescaled next column.
       for (int64_t i = r0 + tid; i < rs; i += QR_THREADS) {
         if (i < j) continue;
-        double* srow = sp + (i - r0) * SROW;
+        double* srow = sp + (i - r0) * SR;
         double row[NBMAX];
 #pragma unroll
         for (int c = 0; c < NBMAX; ++c) row[c] = (c < nb) ? srow[c] : 0.0;
@@ -311,7 +311,7 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
   // write back: P = R (upper) / 0 (below); W = explicit unit-lower Householder vectors
   for (int64_t e = tid; e < (r1 - r0) * nb; e += QR_THREADS) {
     const int64_t il = e % (r1 - r0), c = e / (r1 - r0), i = r0 + il;
-    const double x = in_smem(i) ? sp[il * SROW + c] : P[cm(i, c, ldp)];
+    const double x = in_smem(i) ? sp[il * SR + c] : P[cm(i, c, ldp)];
     P[cm(i, c, ldp)] = i <= c ? x : 0.0;
     W[cm(i, c, ldw)] = i < c ? 0.0 : (i == c ? 1.0 : x);
   }
@@ -336,6 +336,55 @@ void panel_force(int global_variant, int ctas) {
   g_qr_ctas = ctas > 0 ? ctas : 0;
 }
 
+namespace {
+// Shared-memory rows per CTA of the 16-column sub-panel kernel (row stride 17 doubles) within the
+// 227 KB opt-in limit (dynamic + the kernel's ~11 KB static shared memory).
+constexpr int SROW16 = 17;
+constexpr int SMEM_ROWS_MAX16 = 1600;
+
+// One cooperative launch of the sub-panel kernel on columns [j0, j0 + nb) of the panel (rows j0:rows).
+void qr2_launch(cudaStream_t st, int64_t rows, int64_t j0, int nb, double* P, int64_t ldp, double* W, int64_t ldw,
+                double* tau, double* T, int64_t ldt, const PanelWork& pw, bool narrow) {
+  const int64_t R = rows - j0;
+  // one CTA (no grid barrier) up to 768 rows; else ~256+ rows per CTA, at most one per SM
+  static const int env_max = [] { const char* e = std::getenv("UTV_QR_MAXCTAS"); return e ? std::atoi(e) : 0; }();
+  const int cap = g_qr_ctas > 0 ? g_qr_ctas : env_max;
+  const int gmax = cap > 0 ? std::min(cap, pw.num_sms) : std::min(pw.num_sms, 160);
+  const int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (R + 255) / 256));
+  const int64_t Lr = (R + G - 1) / G;
+  // shared-memory rows: all of a CTA's rows (32 columns up to 768 rows per CTA; the 16-column
+  // sub-panels of tall panels up to 1600), or the first SMEM_ROWS_MAX with the rest re-read from
+  // L2 per column (hybrid); the global-memory variant only when forced (UTV_TUNE_QR_GLOBAL)
+  const bool smem = !g_qr_force_global;
+  int64_t Ls = smem ? std::min<int64_t>(Lr, narrow ? SMEM_ROWS_MAX16 : SMEM_ROWS_MAX) : 0;
+  int64_t Rv = R; int nbv = nb; double* Pb = P + cm(j0, j0, ldp); double* Wb = W + cm(j0, j0, ldw);
+  int64_t wtop = j0; double* taub = tau + j0; double* Tb = T + cm(j0, j0, ldt);
+  void* args[] = {&Rv, &nbv, &Pb, (void*)&ldp, &Wb, (void*)&ldw, &wtop, &taub, &Tb, (void*)&ldt,
+                  (void*)&pw.part, (void*)&pw.bar, &Ls};
+  ProfScope prof(st, kProfPanel, 1, 2.0 * (double)R * nb * nb, 16.0 * (double)R * nb);
+  // tag: 0 = global-memory variant, 1 = shared-memory variant, 3 = hybrid, 6 = 16-column shared-memory
+  prof.shape(R, nb, G, !smem ? 0 : (narrow ? 6 : (Ls < Lr ? 3 : 1)));
+  static std::atomic<unsigned long long> attr{0}, attr_h{0}, attr_n{0};
+  ensure_smem_attr(qr2_kernel<true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr);
+  ensure_smem_attr(qr2_kernel<true, true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr_h);
+  ensure_smem_attr(qr2_kernel<true, false, SROW16>, (int)(SMEM_ROWS_MAX16 * SROW16 * sizeof(double)), attr_n);
+  const size_t smem_bytes = smem ? (size_t)Ls * (narrow ? SROW16 : SROW) * sizeof(double) : 0;
+  void* kern = !smem ? (void*)qr2_kernel<false>
+                     : (narrow ? (void*)qr2_kernel<true, false, SROW16>
+                               : (Ls < Lr ? (void*)qr2_kernel<true, true> : (void*)qr2_kernel<true>));
+  UTV_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(QR_THREADS), args, smem_bytes, st));
+}
+
+// Rows per CTA of a sub-panel with R rows (the grid qr2_launch chooses).
+int64_t qr2_rows_per_cta(int64_t R, const PanelWork& pw) {
+  static const int env_max = [] { const char* e = std::getenv("UTV_QR_MAXCTAS"); return e ? std::atoi(e) : 0; }();
+  const int cap = g_qr_ctas > 0 ? g_qr_ctas : env_max;
+  const int gmax = cap > 0 ? std::min(cap, pw.num_sms) : std::min(pw.num_sms, 160);
+  const int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (R + 255) / 256));
+  return (R + G - 1) / G;
+}
+}  // namespace
+
 void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
               double* T, int64_t ldt, const PanelWork& pw) {
   if (w <= 0) return;
@@ -343,32 +392,32 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
   for (int64_t jb = 0; jb < w; jb += NBMAX) {
     const int nb = (int)std::min<int64_t>(NBMAX, w - jb);
     const int64_t R = rows - jb;
-    // one CTA (no grid barrier) up to 1024 rows; else ~256+ rows per CTA, at most one per SM
-    static const int env_max = [] { const char* e = std::getenv("UTV_QR_MAXCTAS"); return e ? std::atoi(e) : 0; }();
-    const int cap = g_qr_ctas > 0 ? g_qr_ctas : env_max;
-    const int gmax = cap > 0 ? std::min(cap, pw.num_sms) : std::min(pw.num_sms, 160);
-    const int G = R <= 768 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (R + 255) / 256));
-    const int64_t Lr = (R + G - 1) / G;
-    // shared-memory rows: all of a CTA's rows, or (taller panels) the first SMEM_ROWS_MAX of them
-    // with the rest re-read from global memory / L2 per column (hybrid); the global-memory variant
-    // only when forced (UTV_TUNE_QR_GLOBAL)
-    const bool smem = !g_qr_force_global;
-    int64_t Ls = smem ? std::min<int64_t>(Lr, SMEM_ROWS_MAX) : 0;
-    int64_t Rv = R; int nbv = nb; double* Pb = P + cm(jb, jb, ldp); double* Wb = W + cm(jb, jb, ldw);
-    int64_t wtop = jb; double* taub = tau + jb; double* Tb = T + cm(jb, jb, ldt);
-    void* args[] = {&Rv, &nbv, &Pb, (void*)&ldp, &Wb, (void*)&ldw, &wtop, &taub, &Tb, (void*)&ldt,
-                    (void*)&pw.part, (void*)&pw.bar, &Ls};
-    {
-      ProfScope prof(st, kProfPanel, 1, 2.0 * (double)R * nb * nb, 16.0 * (double)R * nb);
-      // tag: 0 = global-memory variant, 1 = shared-memory variant, 3 = hybrid (smem head + global tail)
-      prof.shape(R, nb, G, !smem ? 0 : (Ls < Lr ? 3 : 1));
-      static std::atomic<unsigned long long> attr{0};
-      ensure_smem_attr(qr2_kernel<true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr);
-      static std::atomic<unsigned long long> attr_h{0};
-      ensure_smem_attr(qr2_kernel<true, true>, (int)(SMEM_ROWS_MAX * SROW * sizeof(double)), attr_h);
-      const size_t smem_bytes = smem ? (size_t)Ls * SROW * sizeof(double) : 0;
-      void* kern = !smem ? (void*)qr2_kernel<false> : (Ls < Lr ? (void*)qr2_kernel<true, true> : (void*)qr2_kernel<true>);
-      UTV_CUDA(cudaLaunchCooperativeKernel(kern, dim3(G), dim3(QR_THREADS), args, smem_bytes, st));
+    double* Wb = W + cm(jb, jb, ldw);
+    double* Tb = T + cm(jb, jb, ldt);
+    const int64_t Lr = qr2_rows_per_cta(R, pw);
+    if (!g_qr_force_global && Lr > SMEM_ROWS_MAX && Lr <= SMEM_ROWS_MAX16 && nb > 16) {
+      // Tall panel: rows per CTA exceed what 32 columns fit in shared memory but 16 columns fit.
+      // The 32-column sub-panel is factored as two 16-column halves (each entirely in shared memory)
+      // with Q_a^T applied to the second half in between; T_bb = [T_a, -T_a (W_a^T W_b) T_b; 0, T_b].
+      const int na = 16, nc = nb - 16;
+      qr2_launch(st, rows, jb, na, P, ldp, W, ldw, tau, T, ldt, pw, true);
+      double* Pc = P + cm(jb, jb + na, ldp);
+      dgemm(st, true, false, nc, na, R, 1.0, Pc, ldp, Wb, ldw, 0.0, pw.z1, nc, pw.gemm_work, pw.gemm_work_doubles,
+            pw.num_sms);                                                         // Z1^T = P_c^T W_a
+      dgemm(st, false, false, nc, na, na, 1.0, pw.z1, nc, Tb, ldt, 0.0, pw.z2, nc, pw.gemm_work,
+            pw.gemm_work_doubles, pw.num_sms);                                   // Z2^T = Z1^T T_a
+      dgemm(st, false, true, R, nc, na, -1.0, Wb, ldw, pw.z2, nc, 1.0, Pc, ldp, pw.gemm_work,
+            pw.gemm_work_doubles, pw.num_sms);                                   // P_c -= W_a Z2
+      qr2_launch(st, rows, jb + na, nc, P, ldp, W, ldw, tau, T, ldt, pw, true);
+      double* Wc = W + cm(jb, jb + na, ldw);                                    // rows jb.. (zero above jb + na)
+      dgemm(st, true, false, na, nc, R, 1.0, Wb, ldw, Wc, ldw, 0.0, pw.x, na, pw.gemm_work, pw.gemm_work_doubles,
+            pw.num_sms);                                                         // S_ac = W_a^T W_c
+      dgemm(st, false, false, na, nc, nc, 1.0, pw.x, na, T + cm(jb + na, jb + na, ldt), ldt, 0.0, pw.z1, na,
+            pw.gemm_work, pw.gemm_work_doubles, pw.num_sms);                     // S_ac T_c
+      dgemm(st, false, false, na, nc, na, -1.0, Tb, ldt, pw.z1, na, 0.0, T + cm(jb, jb + na, ldt), ldt,
+            pw.gemm_work, pw.gemm_work_doubles, pw.num_sms);                     // -T_a (S_ac T_c)
+    } else {
+      qr2_launch(st, rows, jb, nb, P, ldp, W, ldw, tau, T, ldt, pw, false);
     }
     const int64_t wr = w - jb - nb;
     if (wr > 0) {

@@ -86,26 +86,41 @@ def check_hqr(P, Pd, W, tau, T):
 
 # ---------------------------------------------------------------------------- a3 / a5 at full height
 @pytest.mark.parametrize("m,w", [(110000, 32), (120000, 64), (120000, 256)])
-@pytest.mark.parametrize("variant", ["hybrid", "global"])
+@pytest.mark.parametrize("variant", ["auto", "global"])
 def test_hqr_full_height(utv, h, tmp_path, m, w, variant):
-    """m > 101 376 (rows per CTA > 768, as in every cfg4 panel): automatically the hybrid kernel
-    (each CTA's first 768 rows in shared memory, the rest re-read from L2 per column, tag 3);
-    forced, the global-memory kernel (tag 0)."""
+    """m > 101 376 (rows per CTA > 768, as in every cfg4 panel): automatically each 32-column
+    sub-panel is factored as two 16-column halves held entirely in shared memory (tag 6); forced,
+    the global-memory kernel (tag 0)."""
     rng = np.random.default_rng(m + w)
     P = rng.standard_normal((m, w))
     with utv.tuned(utv.UTV_TUNE_QR_GLOBAL, 1 if variant == "global" else 0):
         h.profile(True)
         Pd, W, tau, T = h.hqr(dev(P))
         recs = [r for r in records(h, tmp_path) if r["family"] == 1]
-    assert recs and all(r["tag"] == (0 if variant == "global" else 3) for r in recs)
+    assert recs and all(r["tag"] == (0 if variant == "global" else 6) for r in recs)
     assert max(r["K"] for r in recs) > 100                                        # cooperative grid
     check_hqr(P, Pd, W, tau, T)
 
 
-@pytest.mark.parametrize("m,w,ctas", [(9000, 64, 7), (9000, 256, 5), (3001, 200, 2), (2000, 33, 2)])
+@pytest.mark.parametrize("m,w,ctas", [(9000, 64, 7), (3001, 200, 2), (2000, 33, 2), (5000, 48, 4)])
+def test_hqr_grouped16_small(utv, h, tmp_path, m, w, ctas):
+    """The 16-column halves (768 < rows per CTA <= 1600, reached here through a CTA cap): Q_a^T
+    applied between the halves and T_bb merged from T_a, T_c and W_a^T W_c; ragged widths (a
+    narrow last sub-panel takes the hybrid kernel)."""
+    rng = np.random.default_rng(17 * m + w + ctas)
+    P = rng.standard_normal((m, w))
+    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas):
+        h.profile(True)
+        Pd, W, tau, T = h.hqr(dev(P))
+        recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    assert recs and any(r["tag"] == 6 for r in recs) and all(r["tag"] in (3, 6) for r in recs)
+    check_hqr(P, Pd, W, tau, T)
+
+
+@pytest.mark.parametrize("m,w,ctas", [(9000, 64, 5), (9000, 256, 5), (6001, 200, 3), (4000, 33, 2)])
 def test_hqr_hybrid_small(utv, h, tmp_path, m, w, ctas):
-    """The hybrid kernel at sizes the oracle factors quickly: a CTA cap leaves more than 768 rows
-    per CTA (shared-memory head + global tail, ragged widths and sub-panels)."""
+    """The hybrid kernel (more than 1600 rows per CTA: the first 768 in shared memory, the rest
+    re-read from L2) at sizes the oracle factors quickly, through a CTA cap."""
     rng = np.random.default_rng(11 * m + w + ctas)
     P = rng.standard_normal((m, w))
     with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas):
@@ -197,11 +212,11 @@ def test_lstsq_n3072_b256_q2_long_k_tiles(utv, h, tmp_path):
     assert any(((r["tag"] >> 2) & 63) == 0 and (r["tag"] & 1) == 1 for r in long_k)     # TN: Y = A'^T Z
 
 
-@pytest.mark.parametrize("variant", ["hybrid", "global"])
+@pytest.mark.parametrize("variant", ["auto", "global"])
 def test_lstsq_tall_panels(utv, h, tmp_path, variant):
     """cfg4's shape family (tall, 16 RHS, q = 1) at m = 120 000 x n = 512: every a5 panel has more
-    than 101 376 rows -- the hybrid kernel (automatic) or the global-memory one (forced) inside
-    the solver."""
+    than 101 376 rows -- the 16-column shared-memory halves (automatic) or the global-memory
+    kernel (forced) inside the solver."""
     M = gen.GpMatrix(120000, 512, 384, seed=32)
     B, X0 = M.known_rhs(k=16)
     Xo, ro = oracle.lstsq(M.A, B, b=256, q=1, tau=1e-10, seed=gen.SKETCH_SEED)
@@ -211,7 +226,7 @@ def test_lstsq_tall_panels(utv, h, tmp_path, variant):
     assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
     assert np.linalg.norm(Xg - X0) <= 1e-10 * np.linalg.norm(X0)
     panels = [r for r in recs if r["family"] == 1 and r["M"] > 101376]
-    assert panels and all(r["tag"] == (0 if variant == "global" else 3) for r in panels)
+    assert panels and all(r["tag"] == (0 if variant == "global" else 6) for r in panels)
 
 
 @pytest.mark.parametrize("cfg", [0, 2, 3])
