@@ -19,6 +19,17 @@
 namespace utv {
 
 __device__ long long g_jac_trace[32 * 8];   // diagnostics (-DUTV_JAC_TRACE): CTA 0 phase clocks
+// diagnostics: %globaltimer at the start and end of CTA 0 of every jacobi_kernel launch (ring of
+// kJacRing), the in-situ execution time of the side-stream SVD (its stream events also count the
+// wait for a free 8-SM cluster slot)
+constexpr int kJacRing = 4096;
+__device__ unsigned long long g_jac_ns[2 * kJacRing];
+__device__ unsigned g_jac_cnt;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 namespace {
 constexpr int JBLK = 16;
 constexpr int JT = 512;
@@ -54,11 +65,16 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
   __shared__ int s_rot;
   __shared__ double s_nrm[2 * JBLK];
   __shared__ int s_done;
+  __shared__ unsigned s_slot;
   const int P = gridDim.x, nblk = 2 * P, c = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   (void)bar;
   const double eps = 0x1.0p-52;
   const double small2 = eps * eps * fro2[0];   // R9b: numerically-zero column floor
+  if (c == 0 && tid == 0) {
+    s_slot = atomicAdd(&g_jac_cnt, 1u) % kJacRing;
+    g_jac_ns[2 * s_slot] = globaltimer_ns();
+  }
 
   int sweep = 0;
   bool converged = false;
@@ -224,6 +240,7 @@ jacobi_kernel(int bw, double* __restrict__ W, double* __restrict__ J, const doub
     if (s_done) { converged = true; break; }
   }
   if (c == 0 && tid == 0) {   // accumulated over the steps of one factorization
+    g_jac_ns[2 * s_slot + 1] = globaltimer_ns();
     atomicMax(info, converged ? sweep + 1 : sweep);
     if (!converged) atomicOr(info + 1, 1);
   }
@@ -342,6 +359,21 @@ void svd_small(cudaStream_t st, int64_t bw64, const double* R, int64_t ldr, doub
 }
 
 }  // namespace utv
+
+// diagnostics only (not part of utv.h): copies min(count, max) (start, end) globaltimer pairs of
+// the most recent jacobi_kernel launches to out (2 * max entries) and returns the launch count
+// since the last reset (reset != 0 zeroes it after the copy); -1 on a CUDA error
+extern "C" int utv_debug_jac_times(unsigned long long* out, int max, int reset) {
+  unsigned cnt = 0;
+  if (cudaMemcpyFromSymbol(&cnt, utv::g_jac_cnt, sizeof(unsigned)) != cudaSuccess) return -1;
+  const int n = (int)std::min<unsigned>(cnt, (unsigned)std::min(max, utv::kJacRing));
+  if (n > 0 && cudaMemcpyFromSymbol(out, utv::g_jac_ns, sizeof(unsigned long long) * 2 * n) != cudaSuccess) return -1;
+  if (reset) {
+    const unsigned z = 0;
+    if (cudaMemcpyToSymbol(utv::g_jac_cnt, &z, sizeof(unsigned)) != cudaSuccess) return -1;
+  }
+  return (int)cnt;
+}
 
 extern "C" int utv_debug_jac_trace(long long* out) {   // diagnostics only (not part of utv.h)
   return (int)cudaMemcpyFromSymbol(out, utv::g_jac_trace, sizeof(long long) * 32 * 8);

@@ -299,6 +299,7 @@ struct utv_handle_s {
   unsigned* bar2 = nullptr;      // grid-barrier state of the SVD side stream
   cudaStream_t side = nullptr;   // a7 (small SVD + its 4 updates) overlaps the next step's sketch
   cudaEvent_t ev_panel = nullptr, ev_svd = nullptr, ev_us = nullptr;
+  cudaEvent_t ev_r = nullptr;     // this step's R is in A11 (a5 done): the side-stream SVD may start
   // multi-GPU overlap: collectives of column chunks run on a communication stream (high priority)
   // while the main stream computes the next chunk; the owner's SVDs may lag up to kLagMax steps
   static constexpr int kChunks = 4, kLagMax = 8;
@@ -658,6 +659,17 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
     }
     // ---- apply transformations from the left ----
     panel_qr(st, mp, bw, Ap, lda, Wu, m, tauu, Tu, b, c.pw);                            // a5 (+R13)
+    // a7's SVD reads only R = A11 and writes only A11 (:= Sigma) and side-stream buffers, which
+    // nothing on the main stream touches before the next step's right update (that waits for
+    // ev_svd): start it now, so that it overlaps this step's left update -- whose short-lived
+    // CTAs free an 8-SM cluster slot quickly -- rather than the next step's long-K sketch GEMMs
+    UTV_CUDA(cudaEventRecord(c.h->ev_r, st));
+    UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_r, 0));
+    double* Vsi = fv ? fv->Vs + (size_t)step * b * b : Vs;                             // V_s (kept if factored)
+    double* Usi = kp ? kp->Us + (size_t)step * b * b                                   // kept until applied
+                     : ((step & 1) ? c.at(L.Us2) : Us);
+    svd_small(sd, bw, Ap, lda, Usi, b, sig, Vsi, b, c.sw);                             // a7
+    launch_set_diag(sd, bw, sig, Ap, lda);
     if (kp) kept_push_u(st, *kp, step, mp, bw, Wu, m, Tu);                              // keep W_U, T_U
     if (nr > 0) {                                                                       // a6, R3
       double* Ar = A + cm(j0, j0 + bw, lda);
@@ -699,18 +711,15 @@ void factor_impl(const Ctx& c, int64_t m, int64_t n, double* A, int64_t lda, dou
       us_pending = false;
       us_applied = true;
     }
-    // ---- small SVD and the four updates ----
-    // a7 on the side stream: it only needs R (this step's panel) and touches A11, A01, A12,
-    // V(:, block), C(block, :), U(:, block).  The next step's sketch, power iterations and
-    // QR(Y) read only the trailing matrix, so they overlap it; the next right update (which
-    // writes A12's rows) waits for ev_svd (reading H5: the updates commute, they must not race).
+    // ---- the four updates of the small SVD ----
+    // a7 on the side stream (the SVD itself was launched after a5): the updates touch A01, A12,
+    // V(:, block), C(block, :), U(:, block), so they wait for this step's main-stream work on
+    // those (C and U left updates, the deferred A12 of step i-1).  The next step's sketch, power
+    // iterations and QR(Y) read only the trailing matrix, so they overlap it; the next right
+    // update (which writes A12's rows) waits for ev_svd (reading H5: the updates commute, they
+    // must not race).
     UTV_CUDA(cudaEventRecord(c.h->ev_panel, st));
     UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_panel, 0));
-    double* Vsi = fv ? fv->Vs + (size_t)step * b * b : Vs;                             // V_s (kept if factored)
-    double* Usi = kp ? kp->Us + (size_t)step * b * b                                   // kept until applied
-                     : ((step & 1) ? c.at(L.Us2) : Us);
-    svd_small(sd, bw, Ap, lda, Usi, b, sig, Vsi, b, c.sw);                             // a7
-    launch_set_diag(sd, bw, sig, Ap, lda);
     if (j0 > 0) {                                                                       // A01 := A01 V_s
       // A01's last b rows were just rotated by the deferred U_s^T of step i-1 (main stream)
       if (us_applied) UTV_CUDA(cudaStreamWaitEvent(sd, c.h->ev_us, 0));
@@ -1967,6 +1976,7 @@ utv_status utv_create(utv_handle* handle, int device, void* stream) {
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_panel, cudaEventDisableTiming));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_svd, cudaEventDisableTiming));
     UTV_CUDA(cudaEventCreateWithFlags(&h->ev_us, cudaEventDisableTiming));
+    UTV_CUDA(cudaEventCreateWithFlags(&h->ev_r, cudaEventDisableTiming));
     UTV_CUDA(cudaStreamCreateWithPriority(&h->cst, cudaStreamNonBlocking, hi));
     for (int q = 0; q < utv_handle_s::kChunks; ++q) {
       UTV_CUDA(cudaEventCreateWithFlags(&h->ev_cq[q], cudaEventDisableTiming));
@@ -2082,6 +2092,7 @@ utv_status utv_destroy(utv_handle h) {
   if (h->ev_panel) cudaEventDestroy(h->ev_panel);
   if (h->ev_svd) cudaEventDestroy(h->ev_svd);
   if (h->ev_us) cudaEventDestroy(h->ev_us);
+  if (h->ev_r) cudaEventDestroy(h->ev_r);
   for (int q = 0; q < utv_handle_s::kChunks; ++q) {
     if (h->ev_cq[q]) cudaEventDestroy(h->ev_cq[q]);
     if (h->ev_cd[q]) cudaEventDestroy(h->ev_cd[q]);
