@@ -82,6 +82,10 @@ utv_status utv_rank_diag(utv_handle handle, int64_t n, const double* d, double t
  *                         chunk's GEMM on the communication stream (0 = automatic: 2)
  *   UTV_TUNE_SVD_LAG      multi-GPU handles: steps (1..8) by which the application of a diagonal
  *                         block's SVD may trail its panel QR (0 = automatic: 1 at P = 1, else 8)
+ *   UTV_TUNE_QR_CHOLQR    a3/a5 panel algorithm: 0 = automatic (CholeskyQR2 + Householder
+ *                         reconstruction on 64-column sub-panels of >= 2048 rows, the Householder
+ *                         sub-panel kernels where it declines; reading R22), 1 = Householder kernels
+ *                         only, 2 = CholeskyQR2 attempted at any panel height
  * Returns UTV_ERR_ARG for an unknown key; *old (if non-NULL) gets the previous value. */
 enum {
   UTV_TUNE_GEMM_CFG = 1,
@@ -90,7 +94,8 @@ enum {
   UTV_TUNE_QR_GLOBAL = 4,
   UTV_TUNE_QR_CTAS = 5,
   UTV_TUNE_DIST_CHUNKS = 6,
-  UTV_TUNE_SVD_LAG = 7
+  UTV_TUNE_SVD_LAG = 7,
+  UTV_TUNE_QR_CHOLQR = 8
 };
 utv_status utv_tune(int key, int64_t value, int64_t* old);
 

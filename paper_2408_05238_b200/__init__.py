@@ -532,7 +532,7 @@ def local_group(nranks: int, devices=None, streams=None) -> list:
 
 
 UTV_TUNE_GEMM_CFG, UTV_TUNE_GEMM_SPLITS, UTV_TUNE_GEMM_PATH, UTV_TUNE_QR_GLOBAL, UTV_TUNE_QR_CTAS = 1, 2, 3, 4, 5
-UTV_TUNE_DIST_CHUNKS, UTV_TUNE_SVD_LAG = 6, 7
+UTV_TUNE_DIST_CHUNKS, UTV_TUNE_SVD_LAG, UTV_TUNE_QR_CHOLQR = 6, 7, 8
 
 
 def tune(key: int, value: int) -> int:

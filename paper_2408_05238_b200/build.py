@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libutv.so")
 BUILD = os.path.join(HERE, "_build")
 
-NVCC_FLAGS = [*(["-DUTV_JAC_TRACE", "-DUTV_QR_TRACE"] if os.environ.get("UTV_TRACE") else []), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+NVCC_FLAGS = [*(["-DUTV_JAC_TRACE", "-DUTV_QR_TRACE", "-DUTV_CQR_TRACE"] if os.environ.get("UTV_TRACE") else []), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", f"-I{os.path.join(ROOT, 'include')}"]
 
 

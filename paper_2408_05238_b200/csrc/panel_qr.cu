@@ -329,11 +329,13 @@ qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __res
 namespace {
 int g_qr_force_global = 0;   // utv_tune(UTV_TUNE_QR_GLOBAL): the global-memory qr2 variant at any size
 int g_qr_ctas = 0;           // utv_tune(UTV_TUNE_QR_CTAS): cap on the cooperative CTAs (0 = automatic)
+int g_qr_cholqr = 0;         // utv_tune(UTV_TUNE_QR_CHOLQR): 0 auto, 1 Householder only, 2 CholeskyQR2 forced
 }  // namespace
 
-void panel_force(int global_variant, int ctas) {
+void panel_force(int global_variant, int ctas, int cholqr) {
   g_qr_force_global = global_variant ? 1 : 0;
   g_qr_ctas = ctas > 0 ? ctas : 0;
+  g_qr_cholqr = (cholqr >= 0 && cholqr <= 2) ? cholqr : 0;
 }
 
 namespace {
@@ -385,12 +387,51 @@ int64_t qr2_rows_per_cta(int64_t R, const PanelWork& pw) {
 }
 }  // namespace
 
-void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
-              double* T, int64_t ldt, const PanelWork& pw) {
-  if (w <= 0) return;
-  launch_set_zero(st, w, w, T, ldt);
-  for (int64_t jb = 0; jb < w; jb += NBMAX) {
-    const int nb = (int)std::min<int64_t>(NBMAX, w - jb);
+namespace {
+// Q_b^T applied from the left to the panel columns right of sub-panel [jb, jb + nb) (rows jb:rows),
+// transposed so the skinny dimension nb is the GEMMs' N: Z1^T = P_r^T W_b ; Z2^T = Z1^T T_b ;
+// P_r -= W_b (Z2^T)^T
+void apply_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int64_t nb, int64_t wr, double* P, int64_t ldp,
+                    const double* W, int64_t ldw, const double* T, int64_t ldt, const PanelWork& pw) {
+  if (wr <= 0) return;
+  const int64_t R = rows - jb;
+  double* Pr = P + cm(jb, jb + nb, ldp);
+  const double* Wb = W + cm(jb, jb, ldw);
+  const double* Tb = T + cm(jb, jb, ldt);
+  dgemm(st, true, false, wr, nb, R, 1.0, Pr, ldp, Wb, ldw, 0.0, pw.z1, wr, pw.gemm_work, pw.gemm_work_doubles,
+        pw.num_sms);
+  dgemm(st, false, false, wr, nb, nb, 1.0, pw.z1, wr, Tb, ldt, 0.0, pw.z2, wr, pw.gemm_work, pw.gemm_work_doubles,
+        pw.num_sms);
+  dgemm(st, false, true, R, wr, nb, -1.0, Wb, ldw, pw.z2, wr, 1.0, Pr, ldp, pw.gemm_work, pw.gemm_work_doubles,
+        pw.num_sms);
+}
+
+// dlarft's off-diagonal blocks of T[c0:c1, c0:c1] from the sub-panel blocks of width bw on its
+// diagonal: Gram S = W^T W (rows c0:rows; W is zero above each column's diagonal), then
+// T[0:jb, blk] = -T[0:jb, 0:jb] (S[0:jb, blk] T_bb) (indices relative to c0).
+void assemble_t(cudaStream_t st, int64_t rows, int64_t c0, int64_t c1, int64_t bw, const double* W, int64_t ldw,
+                double* T, int64_t ldt, const PanelWork& pw) {
+  const int64_t cw = c1 - c0;
+  if (cw <= bw) return;
+  const double* Wc = W + cm(c0, c0, ldw);
+  double* Tc = T + cm(c0, c0, ldt);
+  dgemm(st, true, false, cw, cw, rows - c0, 1.0, Wc, ldw, Wc, ldw, 0.0, pw.gram, cw, pw.gemm_work,
+        pw.gemm_work_doubles, pw.num_sms);
+  for (int64_t jb = bw; jb < cw; jb += bw) {
+    const int64_t nb = std::min<int64_t>(bw, cw - jb);
+    dgemm(st, false, false, jb, nb, nb, 1.0, pw.gram + cm(0, jb, cw), cw, Tc + cm(jb, jb, ldt), ldt, 0.0, pw.x, jb,
+          pw.gemm_work, pw.gemm_work_doubles, pw.num_sms);
+    dgemm(st, false, false, jb, nb, jb, -1.0, Tc, ldt, pw.x, jb, 0.0, Tc + cm(0, jb, ldt), ldt, pw.gemm_work,
+          pw.gemm_work_doubles, pw.num_sms);
+  }
+}
+
+// Householder QR (qr2 sub-panel kernels) of columns [c0, c1) of the panel, rows c0:rows; rows
+// above c0 of W are zeroed by the kernels (wtop), T[c0:c1, c0:c1] assembled.
+void panel_hqr(cudaStream_t st, int64_t rows, int64_t c0, int64_t c1, double* P, int64_t ldp, double* W,
+               int64_t ldw, double* tau, double* T, int64_t ldt, const PanelWork& pw) {
+  for (int64_t jb = c0; jb < c1; jb += NBMAX) {
+    const int nb = (int)std::min<int64_t>(NBMAX, c1 - jb);
     const int64_t R = rows - jb;
     double* Wb = W + cm(jb, jb, ldw);
     double* Tb = T + cm(jb, jb, ldt);
@@ -401,13 +442,7 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
       // with Q_a^T applied to the second half in between; T_bb = [T_a, -T_a (W_a^T W_b) T_b; 0, T_b].
       const int na = 16, nc = nb - 16;
       qr2_launch(st, rows, jb, na, P, ldp, W, ldw, tau, T, ldt, pw, true);
-      double* Pc = P + cm(jb, jb + na, ldp);
-      dgemm(st, true, false, nc, na, R, 1.0, Pc, ldp, Wb, ldw, 0.0, pw.z1, nc, pw.gemm_work, pw.gemm_work_doubles,
-            pw.num_sms);                                                         // Z1^T = P_c^T W_a
-      dgemm(st, false, false, nc, na, na, 1.0, pw.z1, nc, Tb, ldt, 0.0, pw.z2, nc, pw.gemm_work,
-            pw.gemm_work_doubles, pw.num_sms);                                   // Z2^T = Z1^T T_a
-      dgemm(st, false, true, R, nc, na, -1.0, Wb, ldw, pw.z2, nc, 1.0, Pc, ldp, pw.gemm_work,
-            pw.gemm_work_doubles, pw.num_sms);                                   // P_c -= W_a Z2
+      apply_subpanel(st, rows, jb, na, nc, P, ldp, W, ldw, T, ldt, pw);
       qr2_launch(st, rows, jb + na, nc, P, ldp, W, ldw, tau, T, ldt, pw, true);
       double* Wc = W + cm(jb, jb + na, ldw);                                    // rows jb.. (zero above jb + na)
       dgemm(st, true, false, na, nc, R, 1.0, Wb, ldw, Wc, ldw, 0.0, pw.x, na, pw.gemm_work, pw.gemm_work_doubles,
@@ -419,31 +454,41 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
     } else {
       qr2_launch(st, rows, jb, nb, P, ldp, W, ldw, tau, T, ldt, pw, false);
     }
-    const int64_t wr = w - jb - nb;
-    if (wr > 0) {
-      double* Pr = P + cm(jb, jb + nb, ldp);
-      // Apply Q_b^T from the left, transposed so the skinny dimension (nb <= 32) is the GEMMs' N
-      // (the narrow 128 x 32 tile): Z1^T = P_r^T W_b ; Z2^T = Z1^T T_b ; P_r -= W_b (Z2^T)^T
-      dgemm(st, true, false, wr, nb, R, 1.0, Pr, ldp, Wb, ldw, 0.0, pw.z1, wr, pw.gemm_work, pw.gemm_work_doubles,
-            pw.num_sms);
-      dgemm(st, false, false, wr, nb, nb, 1.0, pw.z1, wr, Tb, ldt, 0.0, pw.z2, wr, pw.gemm_work,
-            pw.gemm_work_doubles, pw.num_sms);
-      dgemm(st, false, true, R, wr, nb, -1.0, Wb, ldw, pw.z2, wr, 1.0, Pr, ldp, pw.gemm_work,
-            pw.gemm_work_doubles, pw.num_sms);
-    }
+    apply_subpanel(st, rows, jb, nb, c1 - jb - nb, P, ldp, W, ldw, T, ldt, pw);
   }
-  if (w > NBMAX) {
-    // Gram S = W^T W (upper part used), then T[0:jb, blk] = -T[0:jb,0:jb] (S[0:jb, blk] T_bb)
-    dgemm(st, true, false, w, w, rows, 1.0, W, ldw, W, ldw, 0.0, pw.gram, w, pw.gemm_work, pw.gemm_work_doubles,
-          pw.num_sms);
-    for (int64_t jb = NBMAX; jb < w; jb += NBMAX) {
-      const int64_t nb = std::min<int64_t>(NBMAX, w - jb);
-      dgemm(st, false, false, jb, nb, nb, 1.0, pw.gram + cm(0, jb, w), w, T + cm(jb, jb, ldt), ldt, 0.0, pw.x, jb,
-            pw.gemm_work, pw.gemm_work_doubles, pw.num_sms);
-      dgemm(st, false, false, jb, nb, jb, -1.0, T, ldt, pw.x, jb, 0.0, T + cm(0, jb, ldt), ldt, pw.gemm_work,
-            pw.gemm_work_doubles, pw.num_sms);
-    }
+  assemble_t(st, rows, c0, c1, NBMAX, W, ldw, T, ldt, pw);
+}
+
+// CholeskyQR2 sub-panels from this many rows on (below, the one-CTA / few-CTA Householder kernel
+// is as fast); UTV_CQR_MIN_ROWS overrides (diagnostics)
+int64_t cholqr_min_rows() {
+  static const int64_t v = [] { const char* e = std::getenv("UTV_CQR_MIN_ROWS"); return e ? std::atoll(e) : 2048; }();
+  return v;
+}
+}  // namespace
+
+void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
+              double* T, int64_t ldt, const PanelWork& pw) {
+  if (w <= 0) return;
+  launch_set_zero(st, w, w, T, ldt);
+  // g_qr_cholqr: 0 = automatic (tall sub-panels), 1 = Householder kernels only, 2 = CholeskyQR2 at any height
+  const bool force = g_qr_cholqr == 2;
+  const bool cq = pw.cq && g_qr_cholqr != 1 && !g_qr_force_global && (force || rows >= cholqr_min_rows());
+  if (!cq) {
+    panel_hqr(st, rows, 0, w, P, ldp, W, ldw, tau, T, ldt, pw);
+    return;
   }
+  const int64_t bw = cholqr_max_width();
+  for (int64_t jb = 0; jb < w; jb += bw) {
+    const int nb = (int)std::min<int64_t>(bw, w - jb);
+    // narrow last sub-panels (< 48 columns) are cheaper on the Householder kernels (~6 us per column
+    // against a ~270 us fixed cost of the CholeskyQR2 sequence at 50000 rows)
+    const bool tall = force || (rows - jb >= cholqr_min_rows() && nb >= 48);
+    if (!(tall && cholqr_subpanel(st, rows, jb, nb, P, ldp, W, ldw, tau, T, ldt, pw)))
+      panel_hqr(st, rows, jb, jb + nb, P, ldp, W, ldw, tau, T, ldt, pw);
+    apply_subpanel(st, rows, jb, nb, w - jb - nb, P, ldp, W, ldw, T, ldt, pw);
+  }
+  assemble_t(st, rows, 0, w, bw, W, ldw, T, ldt, pw);
 }
 
 }  // namespace utv

@@ -401,7 +401,7 @@ void ensure_buf(double** p, size_t* have, size_t need) {
 // Workspace layout for one factorization (offsets in doubles).
 struct Layout {
   size_t G, Y, Z, Wv, Tv, tauv, X, X2, Wu, S, Tu, tauu, Z1, Z2, tmp, R, Us, Us2, Vs, sig, sig2;
-  size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve;
+  size_t sW, sJ, sWs, sWh, sTq, sX, sQ, stau, part, pz1, pz2, gram, px, gemm, zsolve, cq, csm;
   size_t part2, pz1b, pz2b, gram2, px2, gemm2, tmp2;
   size_t nM, nW, ntau, nT, nWt, nY, nY2;
   size_t gemm_doubles, gemm2_doubles;
@@ -444,10 +444,12 @@ Layout plan(int64_t m, int64_t n, int64_t k, int64_t b, int num_sms) {
   L.sQ = take((size_t)b * b);
   L.stau = take(b);
   L.part = take((size_t)num_sms * 128);   // 2 buffers x G x (32 sums + 32 pivot values)
-  L.pz1 = take((size_t)32 * b);
-  L.pz2 = take((size_t)32 * b);
+  L.pz1 = take((size_t)64 * b);          // 64-column sub-panels (CholeskyQR2 path)
+  L.pz2 = take((size_t)64 * b);
   L.gram = take((size_t)b * b);
-  L.px = take((size_t)b * 32);
+  L.px = take((size_t)b * 64);
+  L.cq = take((size_t)std::max<int64_t>(mx, n + b) * cholqr_max_width());   // Q_1 of a sub-panel
+  L.csm = take(cholqr_small_doubles());
   L.zsolve = take((size_t)n * std::max<int64_t>(k, 1));
   // split-K partials: the b x b Gram products (<= 128 b^2) and up to 4 splits of the long-K
   // max(m,n) x b sketch products (wave-quantisation fix, see gemm.cu make_plan)
@@ -493,6 +495,14 @@ struct Ctx {
   }
 };
 
+// Host wait of the panel kernels (the CholeskyQR2 accept flag): the communicator's wait on a
+// multi-GPU handle (polls NCCL's asynchronous error state), else a stream synchronisation.
+void panel_wait(void* hp, cudaStream_t st) {
+  utv_handle h = static_cast<utv_handle>(hp);
+  if (h->comm) h->comm->wait(st);
+  else UTV_CUDA(cudaStreamSynchronize(st));
+}
+
 Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
   Ctx c;
   c.h = h;
@@ -509,6 +519,12 @@ Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
   // its SMs, so that all their grids stay co-resident even when launched at the same time.
   c.pw = PanelWork{c.at(L.part), c.at(L.pz1), c.at(L.pz2), c.at(L.gram), c.at(L.px), c.at(L.gemm), L.gemm_doubles,
                    h->bar, std::max(1, (h->num_sms - 16) / h->coop_share)};
+  c.pw.cq = c.at(L.cq);
+  c.pw.csm = c.at(L.csm);
+  c.pw.dflag = h->info + 8;
+  c.pw.hflag = h->h_info + 3;
+  c.pw.wait = panel_wait;
+  c.pw.wait_ctx = h;
   c.pw2 = PanelWork{c.at(L.part2), c.at(L.pz1b), c.at(L.pz2b), c.at(L.gram2), c.at(L.px2), c.at(L.gemm2),
                     L.gemm2_doubles, h->bar2, std::max(1, h->num_sms / h->coop_share)};
   c.sw = SvdWork{c.at(L.sW), c.at(L.sJ), c.at(L.sWs), c.at(L.sWh), c.at(L.sTq), c.at(L.sX), c.at(L.sQ), c.at(L.stau),
@@ -2604,15 +2620,15 @@ utv_status utv_rank(utv_handle h, int64_t n, const double* T, int64_t ldt, doubl
 
 utv_status utv_tune(int key, int64_t value, int64_t* old) {
   static std::mutex mu;
-  static int64_t cur[8] = {0, -1, 0, 0, 0, 0, 0, 0};
+  static int64_t cur[9] = {0, -1, 0, 0, 0, 0, 0, 0, 0};
   std::lock_guard<std::mutex> lk(mu);
-  if (key < UTV_TUNE_GEMM_CFG || key > UTV_TUNE_SVD_LAG) return UTV_ERR_ARG;
+  if (key < UTV_TUNE_GEMM_CFG || key > UTV_TUNE_QR_CHOLQR) return UTV_ERR_ARG;
   if (old) *old = cur[key];
   cur[key] = value;
   if (key == UTV_TUNE_GEMM_CFG && (value < 0 || value > 5)) cur[key] = -1;
   if (key != UTV_TUNE_GEMM_CFG && value < 0) cur[key] = 0;
   dgemm_force((int)cur[UTV_TUNE_GEMM_CFG], (int)cur[UTV_TUNE_GEMM_SPLITS], (int)cur[UTV_TUNE_GEMM_PATH]);
-  panel_force((int)cur[UTV_TUNE_QR_GLOBAL], (int)cur[UTV_TUNE_QR_CTAS]);
+  panel_force((int)cur[UTV_TUNE_QR_GLOBAL], (int)cur[UTV_TUNE_QR_CTAS], (int)cur[UTV_TUNE_QR_CHOLQR]);
   g_dist_chunks = (int)std::min<int64_t>(cur[UTV_TUNE_DIST_CHUNKS], utv_handle_s::kChunks);
   g_svd_lag = (int)std::min<int64_t>(cur[UTV_TUNE_SVD_LAG], utv_handle_s::kLagMax);
   return UTV_OK;

@@ -88,12 +88,13 @@ def check_hqr(P, Pd, W, tau, T):
 @pytest.mark.parametrize("m,w", [(110000, 32), (120000, 64), (120000, 256)])
 @pytest.mark.parametrize("variant", ["auto", "global"])
 def test_hqr_full_height(utv, h, tmp_path, m, w, variant):
-    """m > 101 376 (rows per CTA > 768, as in every cfg4 panel): automatically each 32-column
+    """m > 101 376 (rows per CTA > 768, as in every cfg4 panel), Householder kernels (the
+    CholeskyQR2 path switched off, as for the panels it declines): automatically each 32-column
     sub-panel is factored as two 16-column halves held entirely in shared memory (tag 6); forced,
     the global-memory kernel (tag 0)."""
     rng = np.random.default_rng(m + w)
     P = rng.standard_normal((m, w))
-    with utv.tuned(utv.UTV_TUNE_QR_GLOBAL, 1 if variant == "global" else 0):
+    with utv.tuned(utv.UTV_TUNE_QR_GLOBAL, 1 if variant == "global" else 0, utv.UTV_TUNE_QR_CHOLQR, 1):
         h.profile(True)
         Pd, W, tau, T = h.hqr(dev(P))
         recs = [r for r in records(h, tmp_path) if r["family"] == 1]
@@ -109,7 +110,7 @@ def test_hqr_grouped16_small(utv, h, tmp_path, m, w, ctas):
     narrow last sub-panel takes the hybrid kernel)."""
     rng = np.random.default_rng(17 * m + w + ctas)
     P = rng.standard_normal((m, w))
-    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas):
+    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas, utv.UTV_TUNE_QR_CHOLQR, 1):
         h.profile(True)
         Pd, W, tau, T = h.hqr(dev(P))
         recs = [r for r in records(h, tmp_path) if r["family"] == 1]
@@ -123,7 +124,7 @@ def test_hqr_hybrid_small(utv, h, tmp_path, m, w, ctas):
     re-read from L2) at sizes the oracle factors quickly, through a CTA cap."""
     rng = np.random.default_rng(11 * m + w + ctas)
     P = rng.standard_normal((m, w))
-    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas):
+    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas, utv.UTV_TUNE_QR_CHOLQR, 1):
         h.profile(True)
         Pd, W, tau, T = h.hqr(dev(P))
         recs = [r for r in records(h, tmp_path) if r["family"] == 1]
@@ -151,9 +152,125 @@ def test_hqr_forced_cta_count(utv, h, ctas):
     over a different partition) -- same factors as the oracle."""
     rng = np.random.default_rng(ctas)
     P = rng.standard_normal((9000, 64))
-    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas, utv.UTV_TUNE_QR_GLOBAL, 1):
+    with utv.tuned(utv.UTV_TUNE_QR_CTAS, ctas, utv.UTV_TUNE_QR_GLOBAL, 1, utv.UTV_TUNE_QR_CHOLQR, 1):
         Pd, W, tau, T = h.hqr(dev(P))
     check_hqr(P, Pd, W, tau, T)
+
+
+# ---------------------------------------------------------------------------- a3 / a5: CholeskyQR2 path
+CQR_TAGS = (10, 11)          # cqr_chol_kernel, cqr_recon_kernel
+QR2_TAGS = (0, 1, 3, 6)      # the Householder sub-panel kernels
+
+
+def _cqr_subpanels(m, w):
+    """Sub-panels the automatic choice gives to CholeskyQR2: 64 columns (or a last one of >= 48)
+    with >= 2048 rows (csrc/panel_qr.cu)."""
+    return sum(1 for jb in range(0, w, 64) if min(64, w - jb) >= 48 and m - jb >= 2048)
+
+
+@pytest.mark.parametrize("m,w", [(3000, 64), (5000, 256), (2500, 100), (20000, 200), (50000, 96), (120000, 256),
+                                 (2100, 128)])
+def test_hqr_cholqr_matches_oracle(utv, h, tmp_path, m, w):
+    """Tall panels (>= 2048 rows) take CholeskyQR2 + Householder reconstruction (reading R22) on
+    64-column sub-panels, narrow last sub-panels (< 48 columns) and short ones (< 2048 rows) the
+    Householder kernels: either way the SAME W, tau, T, R as the oracle's dlarfg/dlarft
+    Householder QR (R8) element by element."""
+    rng = np.random.default_rng(5 * m + w)
+    P = rng.standard_normal((m, w))
+    h.profile(True)
+    Pd, W, tau, T = h.hqr(dev(P))
+    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    ncq = _cqr_subpanels(m, w)
+    assert ncq > 0 and sum(r["tag"] == 11 for r in recs) == ncq
+    assert any(r["tag"] in QR2_TAGS for r in recs) == (ncq < (w + 63) // 64)
+    check_hqr(P, Pd, W, tau, T)
+
+
+@pytest.mark.parametrize("m,w", [(64, 64), (129, 33), (300, 130), (700, 256), (1000, 7)])
+def test_hqr_cholqr_forced_small(utv, h, tmp_path, m, w):
+    """The CholeskyQR2 path forced below its row threshold: square and ragged panels, a last
+    sub-panel narrower than 64, m == w (no W_2 rows)."""
+    rng = np.random.default_rng(3 * m + w)
+    P = rng.standard_normal((m, w)) + 2.0 * np.eye(m, w)
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        h.profile(True)
+        Pd, W, tau, T = h.hqr(dev(P))
+        recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    assert sum(r["tag"] == 11 for r in recs) == (w + 63) // 64
+    check_hqr(P, Pd, W, tau, T)
+
+
+def _declining_panel(kind, m, w, rng):
+    P = rng.standard_normal((m, w))
+    if kind == "zero_column":
+        P[:, 70] = 0.0                                    # second sub-panel: tau = 0 (R8)
+    elif kind == "duplicate_column":
+        P[:, 5] = P[:, 3]                                 # first sub-panel rank deficient
+    elif kind == "near_dependent":
+        P[:, 70] = P[:, 69] + 1e-9 * rng.standard_normal(m)    # kappa ~ 1e11: ||Q_1^T Q_1 - I|| check
+    elif kind == "graded":
+        P *= 10.0 ** -np.linspace(0, 9, w)                # kappa ~ 1e9: beyond CholeskyQR2
+    elif kind == "rank_transition":
+        G = rng.standard_normal((m, 100)) @ rng.standard_normal((100, w))
+        P = G + 1e-14 * rng.standard_normal((m, w))       # randUTV's exact-rank transition panel
+    return P
+
+
+@pytest.mark.parametrize("m", [3000, 40000])
+def test_hqr_cholqr_zero_column_declines(utv, h, tmp_path, m):
+    """A zero column makes the sub-panel's Gram matrix singular: the Cholesky pivot check declines
+    it to the Householder kernels (tau = 0 for the zero column, R8) while the other sub-panel keeps
+    CholeskyQR2; the factors equal the oracle's element by element."""
+    rng = np.random.default_rng(m)
+    P = _declining_panel("zero_column", m, 128, rng)
+    h.profile(True)
+    Pd, W, tau, T = h.hqr(dev(P))
+    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    assert any(r["tag"] in QR2_TAGS for r in recs)            # declined ...
+    assert any(r["tag"] == 12 for r in recs)                  # ... and the first sub-panel did not
+    assert host(tau)[70] == 0.0
+    check_hqr(P, Pd, W, tau, T)
+
+
+def test_hqr_cholqr_graded_columns_accepted(utv, h, tmp_path):
+    """Column scaling alone (kappa ~ 1e9 from 10^0 .. 10^-9 column norms) does not hurt
+    CholeskyQR2 -- it is invariant under P -> P D, as Householder QR is -- so such panels keep the
+    fast path and still equal the oracle element by element."""
+    rng = np.random.default_rng(9)
+    P = _declining_panel("graded", 20000, 128, rng)
+    h.profile(True)
+    Pd, W, tau, T = h.hqr(dev(P))
+    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    assert not any(r["tag"] in QR2_TAGS for r in recs)
+    check_hqr(P, Pd, W, tau, T)
+
+
+@pytest.mark.parametrize("kind", ["duplicate_column", "near_dependent", "rank_transition"])
+def test_hqr_cholqr_rank_deficient_panel(utv, h, tmp_path, kind):
+    """Rank-deficient or nearly dependent panels (a repeated column; a column within 1e-9 of its
+    neighbour; numerical rank 100 < w, the block where randUTV crosses the exact rank): the affected
+    sub-panels decline to the Householder kernels.  A
+    reflector built from a rounding-noise column is not unique (any implementation's differs), so
+    the comparison is by what is unique: Q = I - W T W^T orthogonal, Q R = P, |diag R| up to the
+    deficiency equal to the oracle's, R's columns before it element-wise."""
+    rng = np.random.default_rng(77)
+    m, w = 30000, 256
+    P = _declining_panel(kind, m, w, rng)
+    h.profile(True)
+    Pd, W, tau, T = h.hqr(dev(P))
+    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
+    assert any(r["tag"] in QR2_TAGS for r in recs)
+    Rg = np.triu(host(Pd))[:w]
+    Wg, Tg = host(W), host(T)
+    Q = np.eye(m, w) - Wg @ (Tg @ Wg[:w].T)
+    assert np.abs(Q.T @ Q - np.eye(w)).max() <= 1e-12
+    assert np.linalg.norm(Q @ Rg - P) <= 1e-13 * np.linalg.norm(P)
+    Pk, _, _ = oracle.hqr(P)
+    Ro = np.triu(Pk)[:w]
+    ok = {"duplicate_column": 5, "near_dependent": 70, "rank_transition": 100}[kind]   # columns before it
+    scale = np.abs(Ro).max()
+    assert np.abs(Rg[:, :ok] - Ro[:, :ok]).max() <= 1e-12 * scale
+    assert np.abs(np.abs(np.diag(Rg))[:ok] - np.abs(np.diag(Ro))[:ok]).max() <= 1e-12 * scale
 
 
 # ---------------------------------------------------------------------------- the GEMM variants
@@ -220,13 +337,39 @@ def test_lstsq_tall_panels(utv, h, tmp_path, variant):
     M = gen.GpMatrix(120000, 512, 384, seed=32)
     B, X0 = M.known_rhs(k=16)
     Xo, ro = oracle.lstsq(M.A, B, b=256, q=1, tau=1e-10, seed=gen.SKETCH_SEED)
-    with utv.tuned(utv.UTV_TUNE_QR_GLOBAL, 1 if variant == "global" else 0):
+    with utv.tuned(utv.UTV_TUNE_QR_GLOBAL, 1 if variant == "global" else 0, utv.UTV_TUNE_QR_CHOLQR, 1):
         Xg, rg, recs = _lstsq_profiled(utv, h, tmp_path, M.A, B, 256, 1, gen.SKETCH_SEED)
     assert rg == ro == 384
     assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
     assert np.linalg.norm(Xg - X0) <= 1e-10 * np.linalg.norm(X0)
     panels = [r for r in recs if r["family"] == 1 and r["M"] > 101376]
     assert panels and all(r["tag"] == (0 if variant == "global" else 6) for r in panels)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("gen_kind", ["gp", "gd"])
+def test_lstsq_panel_algorithm(utv, h, tmp_path, mode, gen_kind):
+    """The whole solver with the a3/a5 panels on the Householder kernels only (mode 1) or with
+    CholeskyQR2 attempted on every sub-panel (mode 2; the exact-rank transition and the sketches
+    of a decaying spectrum decline to Householder): x to 1e-9 of the oracle, r identical."""
+    if gen_kind == "gp":
+        M = gen.GpMatrix(1500, 1200, 700, seed=41)
+        A = M.A
+        B, _ = M.known_rhs(k=2)
+    else:
+        M = gen.GdMatrix(1500, 1200, 700, alpha=3, seed=42)
+        A = M.A
+        B, _ = M.known_rhs(k=2)
+    Xo, ro = oracle.lstsq(A, B, b=128, q=2, tau=1e-10, seed=4)
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, mode):
+        Xg, rg, recs = _lstsq_profiled(utv, h, tmp_path, A, B, 128, 2, 4)
+    assert rg == ro == 700
+    assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
+    tags = {r["tag"] for r in recs if r["family"] == 1}
+    if mode == 1:
+        assert not tags & set(CQR_TAGS)
+    else:
+        assert 11 in tags
 
 
 @pytest.mark.parametrize("cfg", [0, 2, 3])

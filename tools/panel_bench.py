@@ -1,4 +1,6 @@
-"""Latency of the panel QR (utv_hqr) and the small SVD (utv_svd_small) at randUTV's shapes."""
+"""Latency of the panel QR (utv_hqr) at randUTV's shapes, per panel algorithm (utv_tune
+UTV_TUNE_QR_CHOLQR: 0 automatic = CholeskyQR2 on tall sub-panels, 1 = Householder kernels only),
+and of the small SVD (utv_svd_small).  Writes gpurun_out/panel_bench.json."""
 import sys, json
 import torch
 sys.path.insert(0, ".")
@@ -13,13 +15,18 @@ def timeit(f, reps=5):
         e0.record(); f(); e1.record(); torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
     return best
-for m, w in ((50000, 256), (20000, 256), (2000, 256), (256, 256), (50000, 32)):
-    P0 = utv.colmajor_empty(m, w); P0.normal_()
-    P = P0.clone()
-    def f():
-        P.copy_(P0); h.hqr(P)
-    res[f"hqr_{m}x{w}_ms"] = timeit(f)
-    print(f"hqr {m}x{w}", res[f"hqr_{m}x{w}_ms"], "ms", flush=True)
+shapes = ((200000, 256), (100000, 256), (50000, 256), (20000, 256), (5000, 256), (2048, 256), (1024, 256),
+          (256, 256), (50000, 32))
+for mode, name in ((1, "householder"), (0, "auto")):
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, mode):
+        for m, w in shapes:
+            P0 = utv.colmajor_empty(m, w); P0.normal_()
+            P = P0.clone()
+            def f():
+                P.copy_(P0); h.hqr(P)
+            key = f"hqr_{name}_{m}x{w}_ms"
+            res[key] = timeit(f)
+            print(key, round(res[key], 4), flush=True)
 torch.manual_seed(5)
 R = torch.triu(torch.randn(256, 256, dtype=torch.float64, device="cuda")).t().contiguous().t()
 def g():
