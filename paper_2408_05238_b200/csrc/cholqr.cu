@@ -33,6 +33,9 @@ constexpr int CQ_THREADS = 256;
 
 // diagnostics: %globaltimer at the phase boundaries of cqr_recon_kernel (build with -DUTV_CQR_TRACE)
 __device__ long long g_cqr_trace[16];
+// diagnostics: sub-panels attempted / accepted by the CholeskyQR2 path on this device (tests read them
+// through utv_debug_cqr_stats to see which sub-panels declined to the Householder kernels)
+__device__ unsigned long long g_cqr_stats[2];
 #ifdef UTV_CQR_TRACE
 #define CQ_TRACE(k) do { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_cqr_trace[k] = t_; } } while (0)
 #else
@@ -218,7 +221,10 @@ cqr_chol_kernel(int nb, const double* __restrict__ G, int64_t ldg, double* __res
   __shared__ double pv[CQ_NB];
   load_cm(G, ldg, nb, a);
   const bool ok = lu_fast<false>(a, nb, nullptr, pv) == 0;
-  if (threadIdx.x == 0) *flag = ok ? 0 : 1;
+  if (threadIdx.x == 0) {
+    *flag = ok ? 0 : 1;
+    atomicAdd(&g_cqr_stats[0], 1ull);
+  }
   if (!ok) return;
   lu_to_chol(a, nb);
   for (int e = threadIdx.x; e < nb * nb; e += CQ_THREADS) {
@@ -375,6 +381,7 @@ cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const doubl
     const int r = e % nb, c = e / nb;
     Mout[e] = m[r * CQ_LD + c];
   }
+  if (tid == 0) atomicAdd(&g_cqr_stats[1], 1ull);
   CQ_TRACE(4);
 }
 
@@ -384,10 +391,11 @@ int cholqr_max_width() { return CQ_NB; }
 
 size_t cholqr_small_doubles() { return 3 * (size_t)CQ_NB * CQ_NB; }
 
-// Factor columns [jb, jb + nb) of the panel (rows jb:rows) by CholeskyQR2 + reconstruction.
-// Returns false -- with P, W, T, tau untouched -- when the sub-panel is too ill-conditioned (the
-// caller then uses the Householder kernels).  One host wait per call (the accept / reject flag).
-bool cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* P, int64_t ldp, double* W,
+// Enqueue the CholeskyQR2 + reconstruction of columns [jb, jb + nb) of the panel (rows jb:rows).
+// On the device, pw.dflag ends 0 (accepted: P, W, T, tau written) or nonzero (declined: nothing of
+// P, W, T, tau written); the caller enqueues the Householder kernels under PredScope(pw.dflag, 1),
+// so no host wait is needed.
+void cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* P, int64_t ldp, double* W,
                      int64_t ldw, double* tau, double* T, int64_t ldt, const PanelWork& pw) {
   const int64_t R = rows - jb;
   double* Pb = P + cm(jb, jb, ldp);
@@ -423,9 +431,6 @@ bool cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* 
                                                    T + cm(jb, jb, ldt), ldt, M);
     UTV_CUDA(cudaGetLastError());
   }
-  UTV_CUDA(cudaMemcpyAsync(pw.hflag, pw.dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  pw.wait(pw.wait_ctx, st);
-  if (*(volatile int*)pw.hflag != 0) return false;
   if (R > nb) {
     ProfScope prof(st, kProfPanel, 1, (double)(R - nb) * nb * nb, 16.0 * (double)(R - nb) * nb);
     prof.shape(R - nb, nb, 1, 12);
@@ -433,13 +438,25 @@ bool cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* 
     cqr_trsm_kernel<<<(unsigned)blocks, TRSM_THREADS, 0, st>>>(R - nb, nb, Pb + nb, ldp, M, nb, Wb + nb, ldw,
                                                                pw.dflag);    // W_2 = P_2 (U' R)^{-1}
     UTV_CUDA(cudaGetLastError());
+    PredScope accepted(pw.dflag, 0);
     launch_set_zero(st, R - nb, nb, Pb + nb, ldp);
   }
-  return true;
 }
 
 }  // namespace utv
 
 extern "C" int utv_debug_cqr_trace(long long* out) {   // diagnostics only (not part of utv.h)
   return (int)cudaMemcpyFromSymbol(out, utv::g_cqr_trace, sizeof(long long) * 16);
+}
+
+// diagnostics only (not part of utv.h): out[0] = sub-panels attempted, out[1] = accepted by the
+// CholeskyQR2 path on the current device since the last reset (synchronises the device)
+extern "C" int utv_debug_cqr_stats(unsigned long long* out, int reset) {
+  int e = (int)cudaDeviceSynchronize();
+  if (!e && out) e = (int)cudaMemcpyFromSymbol(out, utv::g_cqr_stats, sizeof(unsigned long long) * 2);
+  if (!e && reset) {
+    const unsigned long long z[2] = {0, 0};
+    e = (int)cudaMemcpyToSymbol(utv::g_cqr_stats, z, sizeof(z));
+  }
+  return e;
 }

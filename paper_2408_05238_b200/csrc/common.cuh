@@ -43,6 +43,25 @@ inline void ensure_smem_attr(K kern, int bytes, std::atomic<unsigned long long>&
   done.fetch_or(bit, std::memory_order_release);
 }
 
+// Device-side launch predicate.  The panel factorization enqueues both of its algorithms for a
+// sub-panel (CholeskyQR2 and the Householder kernels) and lets a device flag written by the
+// CholeskyQR2 check choose, so the host never waits for it: a kernel launched while a PredScope is
+// active on the launching thread runs only if (*flag != 0) == want, otherwise every CTA returns at
+// entry (before touching shared state such as a grid barrier).  flag == nullptr: always runs.
+struct Pred {
+  const int* flag;
+  int want;
+};
+Pred launch_pred();                           // the calling thread's current predicate
+struct PredScope {
+  Pred old;
+  PredScope(const int* flag, int want);
+  ~PredScope();
+};
+__device__ __forceinline__ bool pred_skip(Pred p) {
+  return p.flag && ((*(volatile const int*)p.flag != 0) != (p.want != 0));
+}
+
 // Column-major element access.
 __host__ __device__ __forceinline__ size_t cm(int64_t i, int64_t j, int64_t ld) {
   return (size_t)i + (size_t)j * (size_t)ld;

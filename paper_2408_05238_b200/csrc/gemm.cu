@@ -147,7 +147,8 @@ template <bool TA, bool TB, int VEC, int ID>
 __global__ void __launch_bounds__(Cfg<TA, TB, ID>::THREADS, Cfg<TA, TB, ID>::CTAS_PER_SM)
 dgemm_dmma_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
                   const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-                  int64_t k_chunk, double* __restrict__ partial) {
+                  int64_t k_chunk, double* __restrict__ partial, Pred pr) {
+  if (pred_skip(pr)) return;
   using CF = Cfg<TA, TB, ID>;
   constexpr int BM = CF::BM, BN = CF::BN, THREADS = CF::THREADS, STAGES = CF::STAGES;
   constexpr int WN = CF::WN, MI = CF::MI, NJ = CF::NJ, WTM = 16 * MI, WTN = 8 * NJ;
@@ -388,7 +389,8 @@ template <bool TA, bool TB, int ID>
 __global__ void __launch_bounds__(TmaCfg<TA, TB, ID>::THREADS, TmaCfg<TA, TB, ID>::CTAS_PER_SM)
 dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
                  int64_t N, int64_t K, double alpha, double beta, double* __restrict__ C, int64_t ldc,
-                 int64_t k_chunk, double* __restrict__ partial, int mn_3d) {
+                 int64_t k_chunk, double* __restrict__ partial, int mn_3d, Pred pr) {
+  if (pred_skip(pr)) return;
   using CF = TmaCfg<TA, TB, ID>;
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES;
   constexpr int WN = CF::WN, MI = CF::MI, NJ = CF::NJ, WTM = 16 * MI, WTN = 8 * NJ;
@@ -551,7 +553,8 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
 // C = alpha * sum_{z=0}^{S-1} partial[z] + beta * C, summed in order z = 0..S-1.
 __global__ void dgemm_splitk_reduce(int64_t M, int64_t N, int S, double alpha, const double* __restrict__ partial,
-                                    double beta, double* __restrict__ C, int64_t ldc) {
+                                    double beta, double* __restrict__ C, int64_t ldc, Pred pr) {
+  if (pred_skip(pr)) return;
   const int64_t total = M * N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -572,7 +575,7 @@ void launch_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, co
   auto kern = dgemm_dmma_kernel<TA, TB, VEC, ID>;
   ensure_smem_attr(kern, (int)CF::SMEM, attr_set);
   dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + CF::BM - 1) / CF::BM)), 1u, (unsigned)splits);
-  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial);
+  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kc, partial, launch_pred());
   UTV_CUDA(cudaGetLastError());
 }
 
@@ -639,7 +642,8 @@ bool launch_tma_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   auto kern = dgemm_tma_kernel<TA, TB, ID>;
   ensure_smem_attr(kern, (int)CF::SMEM, attr_set);
   dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + CF::BM - 1) / CF::BM)), 1u, (unsigned)splits);
-  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(ta_map, tb_map, M, N, K, alpha, beta, C, ldc, kc, partial, mn_3d);
+  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(ta_map, tb_map, M, N, K, alpha, beta, C, ldc, kc, partial, mn_3d,
+                                            launch_pred());
   UTV_CUDA(cudaGetLastError());
   return true;
 }
@@ -752,7 +756,7 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
     // C = beta * C (K == 0): reuse the reduce kernel with S = 0
     ProfScope prof(st, kProfMisc, 1, 0.0, 16.0 * (double)M * N);
     dgemm_splitk_reduce<<<std::max<int64_t>(1, std::min<int64_t>((M * N + 255) / 256, 4096)), 256, 0, st>>>(
-        M, N, 0, 0.0, nullptr, beta, C, ldc);
+        M, N, 0, 0.0, nullptr, beta, C, ldc, launch_pred());
     UTV_CUDA(cudaGetLastError());
     return;
   }
@@ -803,7 +807,7 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, d
   if (splits > 1) {
     const int64_t total = M * N;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * (int64_t)num_sms);
-    dgemm_splitk_reduce<<<blocks, 256, 0, st>>>(M, N, splits, alpha, partial, beta, C, ldc);
+    dgemm_splitk_reduce<<<blocks, 256, 0, st>>>(M, N, splits, alpha, partial, beta, C, ldc, launch_pred());
     UTV_CUDA(cudaGetLastError());
   }
 }

@@ -24,21 +24,18 @@ struct PanelWork {
   // CholeskyQR2 + reconstruction path (cholqr.cu); cq == nullptr disables it (side stream)
   double* cq = nullptr;  // >= rows * 64 doubles (Q_1 of a sub-panel)
   double* csm = nullptr; // >= cholqr_small_doubles()
-  int* dflag = nullptr;  // device accept / reject flag
-  int* hflag = nullptr;  // pinned host copy
-  void (*wait)(void*, cudaStream_t) = nullptr;   // host wait for the stream (multi-GPU aware)
-  void* wait_ctx = nullptr;
+  int* dflag = nullptr;  // device accept / reject flag (selects the algorithm on the device)
 };
 // In place: P (rows x w) -> R (upper triangle), zeros strictly below; W (rows x w) the explicit
 // unit-lower Householder vectors; tau (w); T (w x w, upper, zeros below) with
 // Q = H_0 ... H_{w-1} = I - W T W^T.  Requires rows >= w.
 // utv_tune knobs: force the global-memory sub-panel kernel; cap the cooperative CTAs (0 = auto)
 void panel_force(int global_variant, int ctas, int cholqr = 0);
-// CholeskyQR2 + Householder reconstruction of columns [jb, jb + nb) (cholqr.cu, reading R22);
-// false (nothing written) when the sub-panel is too ill-conditioned for it.
+// CholeskyQR2 + Householder reconstruction of columns [jb, jb + nb) (cholqr.cu, reading R22),
+// enqueued; *pw.dflag on the device ends 0 (accepted) or nonzero (declined, nothing written).
 int cholqr_max_width();
 size_t cholqr_small_doubles();
-bool cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* P, int64_t ldp, double* W,
+void cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* P, int64_t ldp, double* W,
                      int64_t ldw, double* tau, double* T, int64_t ldt, const PanelWork& pw);
 void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, double* W, int64_t ldw, double* tau,
               double* T, int64_t ldt, const PanelWork& pw);

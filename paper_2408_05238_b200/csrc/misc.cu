@@ -6,6 +6,13 @@
 namespace utv {
 
 namespace {
+thread_local Pred t_pred{nullptr, 0};
+}  // namespace
+Pred launch_pred() { return t_pred; }
+PredScope::PredScope(const int* flag, int want) : old(t_pred) { t_pred = Pred{flag, want}; }
+PredScope::~PredScope() { t_pred = old; }
+
+namespace {
 __global__ void set_identity_kernel(int64_t rows, int64_t cols, double* A, int64_t lda) {
   const int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -13,7 +20,8 @@ __global__ void set_identity_kernel(int64_t rows, int64_t cols, double* A, int64
     A[cm(i, j, lda)] = i == j ? 1.0 : 0.0;
   }
 }
-__global__ void set_zero_kernel(int64_t rows, int64_t cols, double* A, int64_t lda) {
+__global__ void set_zero_kernel(int64_t rows, int64_t cols, double* A, int64_t lda, Pred pr) {
+  if (pred_skip(pr)) return;
   const int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e % rows, j = e / rows;
@@ -63,7 +71,7 @@ void launch_set_identity(cudaStream_t st, int64_t rows, int64_t cols, double* A,
 void launch_set_zero(cudaStream_t st, int64_t rows, int64_t cols, double* A, int64_t lda) {
   if (rows * cols <= 0) return;
   ProfScope prof(st, kProfMisc, 1, 0.0, 8.0 * (double)(rows * cols));
-  set_zero_kernel<<<grid_for(rows * cols), 256, 0, st>>>(rows, cols, A, lda);
+  set_zero_kernel<<<grid_for(rows * cols), 256, 0, st>>>(rows, cols, A, lda, launch_pred());
   UTV_CUDA(cudaGetLastError());
 }
 void launch_set_diag(cudaStream_t st, int64_t bw, const double* sigma, double* A, int64_t lda) {

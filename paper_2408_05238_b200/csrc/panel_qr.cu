@@ -79,7 +79,8 @@ template <bool SMEM, bool HYB = false, int SR = SROW>
 __global__ void __launch_bounds__(QR_THREADS, 1)
 qr2_kernel(int64_t R, int nb, double* __restrict__ P, int64_t ldp, double* __restrict__ W, int64_t ldw, int64_t wtop,
            double* __restrict__ tau, double* __restrict__ T, int64_t ldt, double* __restrict__ part,
-           unsigned* __restrict__ bar, int64_t Ls) {
+           unsigned* __restrict__ bar, int64_t Ls, Pred pr) {
+  if (pred_skip(pr)) return;                 // uniform: every CTA returns before the grid barrier state
   // SMEM: the first Ls rows of each CTA's range live in shared memory for the whole kernel, the
   // rest (tall panels: hybrid) are re-read from global memory / L2 per column; !SMEM: Ls = 0.
   extern __shared__ double sp[];             // [Ls][SR] (SMEM only)
@@ -361,8 +362,9 @@ void qr2_launch(cudaStream_t st, int64_t rows, int64_t j0, int nb, double* P, in
   int64_t Ls = smem ? std::min<int64_t>(Lr, narrow ? SMEM_ROWS_MAX16 : SMEM_ROWS_MAX) : 0;
   int64_t Rv = R; int nbv = nb; double* Pb = P + cm(j0, j0, ldp); double* Wb = W + cm(j0, j0, ldw);
   int64_t wtop = j0; double* taub = tau + j0; double* Tb = T + cm(j0, j0, ldt);
+  Pred pr = launch_pred();
   void* args[] = {&Rv, &nbv, &Pb, (void*)&ldp, &Wb, (void*)&ldw, &wtop, &taub, &Tb, (void*)&ldt,
-                  (void*)&pw.part, (void*)&pw.bar, &Ls};
+                  (void*)&pw.part, (void*)&pw.bar, &Ls, &pr};
   ProfScope prof(st, kProfPanel, 1, 2.0 * (double)R * nb * nb, 16.0 * (double)R * nb);
   // tag: 0 = global-memory variant, 1 = shared-memory variant, 3 = hybrid, 6 = 16-column shared-memory
   prof.shape(R, nb, G, !smem ? 0 : (narrow ? 6 : (Ls < Lr ? 3 : 1)));
@@ -484,8 +486,15 @@ void panel_qr(cudaStream_t st, int64_t rows, int64_t w, double* P, int64_t ldp, 
     // narrow last sub-panels (< 48 columns) are cheaper on the Householder kernels (~6 us per column
     // against a ~270 us fixed cost of the CholeskyQR2 sequence at 50000 rows)
     const bool tall = force || (rows - jb >= cholqr_min_rows() && nb >= 48);
-    if (!(tall && cholqr_subpanel(st, rows, jb, nb, P, ldp, W, ldw, tau, T, ldt, pw)))
+    if (tall) {
+      // both algorithms enqueued, the device flag picks one: no host wait (the Householder kernels
+      // of a sub-panel CholeskyQR2 accepted return at entry, ~3 us per launch)
+      cholqr_subpanel(st, rows, jb, nb, P, ldp, W, ldw, tau, T, ldt, pw);
+      PredScope declined(pw.dflag, 1);
       panel_hqr(st, rows, jb, jb + nb, P, ldp, W, ldw, tau, T, ldt, pw);
+    } else {
+      panel_hqr(st, rows, jb, jb + nb, P, ldp, W, ldw, tau, T, ldt, pw);
+    }
     apply_subpanel(st, rows, jb, nb, w - jb - nb, P, ldp, W, ldw, T, ldt, pw);
   }
   assemble_t(st, rows, 0, w, bw, W, ldw, T, ldt, pw);

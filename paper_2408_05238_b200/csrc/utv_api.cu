@@ -495,14 +495,6 @@ struct Ctx {
   }
 };
 
-// Host wait of the panel kernels (the CholeskyQR2 accept flag): the communicator's wait on a
-// multi-GPU handle (polls NCCL's asynchronous error state), else a stream synchronisation.
-void panel_wait(void* hp, cudaStream_t st) {
-  utv_handle h = static_cast<utv_handle>(hp);
-  if (h->comm) h->comm->wait(st);
-  else UTV_CUDA(cudaStreamSynchronize(st));
-}
-
 Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
   Ctx c;
   c.h = h;
@@ -521,10 +513,10 @@ Ctx make_ctx(utv_handle h, int64_t m, int64_t n, int64_t k, int64_t b) {
                    h->bar, std::max(1, (h->num_sms - 16) / h->coop_share)};
   c.pw.cq = c.at(L.cq);
   c.pw.csm = c.at(L.csm);
-  c.pw.dflag = h->info + 8;
-  c.pw.hflag = h->h_info + 3;
-  c.pw.wait = panel_wait;
-  c.pw.wait_ctx = h;
+  // info[0..1]: Jacobi sweeps / status, info[2 .. 2 + kMaxSweeps): its per-sweep rotation counts
+  // (side stream); the CholeskyQR2 accept flag of the main-stream panels lives past them
+  static_assert(2 + kMaxSweeps <= 48, "info layout");
+  c.pw.dflag = h->info + 48;
   c.pw2 = PanelWork{c.at(L.part2), c.at(L.pz1b), c.at(L.pz2b), c.at(L.gram2), c.at(L.px2), c.at(L.gemm2),
                     L.gemm2_doubles, h->bar2, std::max(1, h->num_sms / h->coop_share)};
   c.sw = SvdWork{c.at(L.sW), c.at(L.sJ), c.at(L.sWs), c.at(L.sWh), c.at(L.sTq), c.at(L.sX), c.at(L.sQ), c.at(L.stau),

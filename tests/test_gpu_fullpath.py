@@ -162,6 +162,16 @@ CQR_TAGS = (10, 11)          # cqr_chol_kernel, cqr_recon_kernel
 QR2_TAGS = (0, 1, 3, 6)      # the Householder sub-panel kernels
 
 
+def cqr_stats(utv):
+    """(attempted, accepted) CholeskyQR2 sub-panels since the last call (device counters read by
+    utv_debug_cqr_stats).  Both algorithms are enqueued for an attempted sub-panel and a device
+    flag picks one, so the launch records alone do not show which one computed the result."""
+    import ctypes as C
+    buf = (C.c_ulonglong * 2)()
+    assert utv.lib().utv_debug_cqr_stats(buf, 1) == 0
+    return int(buf[0]), int(buf[1])
+
+
 def _cqr_subpanels(m, w):
     """Sub-panels the automatic choice gives to CholeskyQR2: 64 columns (or a last one of >= 48)
     with >= 2048 rows (csrc/panel_qr.cu)."""
@@ -177,12 +187,13 @@ def test_hqr_cholqr_matches_oracle(utv, h, tmp_path, m, w):
     Householder QR (R8) element by element."""
     rng = np.random.default_rng(5 * m + w)
     P = rng.standard_normal((m, w))
+    cqr_stats(utv)
     h.profile(True)
     Pd, W, tau, T = h.hqr(dev(P))
     recs = [r for r in records(h, tmp_path) if r["family"] == 1]
     ncq = _cqr_subpanels(m, w)
     assert ncq > 0 and sum(r["tag"] == 11 for r in recs) == ncq
-    assert any(r["tag"] in QR2_TAGS for r in recs) == (ncq < (w + 63) // 64)
+    assert cqr_stats(utv) == (ncq, ncq)                        # every attempted sub-panel accepted
     check_hqr(P, Pd, W, tau, T)
 
 
@@ -192,11 +203,16 @@ def test_hqr_cholqr_forced_small(utv, h, tmp_path, m, w):
     sub-panel narrower than 64, m == w (no W_2 rows)."""
     rng = np.random.default_rng(3 * m + w)
     P = rng.standard_normal((m, w)) + 2.0 * np.eye(m, w)
+    cqr_stats(utv)
     with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
         h.profile(True)
         Pd, W, tau, T = h.hqr(dev(P))
         recs = [r for r in records(h, tmp_path) if r["family"] == 1]
     assert sum(r["tag"] == 11 for r in recs) == (w + 63) // 64
+    att, acc = cqr_stats(utv)
+    assert att == (w + 63) // 64
+    # a square panel's last column has nothing below its diagonal (dlarfg: tau = 0): declined
+    assert acc == att - (1 if m == w else 0)
     check_hqr(P, Pd, W, tau, T)
 
 
@@ -223,11 +239,9 @@ def test_hqr_cholqr_zero_column_declines(utv, h, tmp_path, m):
     CholeskyQR2; the factors equal the oracle's element by element."""
     rng = np.random.default_rng(m)
     P = _declining_panel("zero_column", m, 128, rng)
-    h.profile(True)
+    cqr_stats(utv)
     Pd, W, tau, T = h.hqr(dev(P))
-    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
-    assert any(r["tag"] in QR2_TAGS for r in recs)            # declined ...
-    assert any(r["tag"] == 12 for r in recs)                  # ... and the first sub-panel did not
+    assert cqr_stats(utv) == (2, 1)                           # the second sub-panel declined
     assert host(tau)[70] == 0.0
     check_hqr(P, Pd, W, tau, T)
 
@@ -238,10 +252,9 @@ def test_hqr_cholqr_graded_columns_accepted(utv, h, tmp_path):
     fast path and still equal the oracle element by element."""
     rng = np.random.default_rng(9)
     P = _declining_panel("graded", 20000, 128, rng)
-    h.profile(True)
+    cqr_stats(utv)
     Pd, W, tau, T = h.hqr(dev(P))
-    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
-    assert not any(r["tag"] in QR2_TAGS for r in recs)
+    assert cqr_stats(utv) == (2, 2)
     check_hqr(P, Pd, W, tau, T)
 
 
@@ -256,10 +269,10 @@ def test_hqr_cholqr_rank_deficient_panel(utv, h, tmp_path, kind):
     rng = np.random.default_rng(77)
     m, w = 30000, 256
     P = _declining_panel(kind, m, w, rng)
-    h.profile(True)
+    cqr_stats(utv)
     Pd, W, tau, T = h.hqr(dev(P))
-    recs = [r for r in records(h, tmp_path) if r["family"] == 1]
-    assert any(r["tag"] in QR2_TAGS for r in recs)
+    att, acc = cqr_stats(utv)
+    assert att == 4 and acc < att
     Rg = np.triu(host(Pd))[:w]
     Wg, Tg = host(W), host(T)
     Q = np.eye(m, w) - Wg @ (Tg @ Wg[:w].T)

@@ -30,7 +30,7 @@ def local_cols(n, b, P, p):
     return utv.dist_local_cols(n, b, P, p)
 
 
-def replay_rank(h, ws, m, n, b, q, k, P, p, nch):
+def replay_rank(h, ws, src, m, n, b, q, k, P, p, nch):
     """Enqueue rank p's kernel sequence; returns per-step lists of phase events."""
     L = utv.lib()
     st = h.stream
@@ -60,8 +60,16 @@ def replay_rank(h, ws, m, n, b, q, k, P, p, nch):
         if st_ != 0:
             raise RuntimeError(f"utv_gemm {ta}{tb} {M}x{N}x{K}: {st_}")
 
+    def refresh(addr, cnt):
+        # a dense random panel before every panel QR: the factorization overwrites its input with R
+        # (zeros below), and the CholeskyQR2 path declines such panels (tau = 0 columns), so
+        # re-factoring the same buffer would time both algorithms (a ~30 us D2D copy at 50000 x 256)
+        i0 = (addr - base) // 8
+        ws[i0:i0 + cnt].copy_(src[:cnt])
+
     def hqr(rows, w):
         # the owner's panel QR (m' x bw) on a scratch panel of the same shape
+        refresh(Pq, rows * w)
         h.check(L.utv_hqr(h.h, rows, w, C.c_void_p(Pq), rows, C.c_void_p(Wu), rows, C.c_void_p(tu), C.c_void_p(Tu), b))
 
     steps = []
@@ -97,6 +105,7 @@ def replay_rank(h, ws, m, n, b, q, k, P, p, nch):
         mark("pre")
         if right:
             # QR(Y) (n' x b), identical on every rank
+            refresh(Y, np_ * b)
             h.check(L.utv_hqr(h.h, np_, b, C.c_void_p(Y), np_, C.c_void_p(Wv), np_, C.c_void_p(tv), C.c_void_p(Tv), b))
         mark("qry")
         if right:
@@ -174,11 +183,12 @@ def main():
         nloc0 = local_cols(n, b, P, 0)
         need = m * max(nloc0, 1) + 40 * max(m, n) * b + 64 * b * b
         ws = torch.randn(need, dtype=torch.float64, device="cuda") * 1e-3
+        src = torch.randn(max(m, n) * b, dtype=torch.float64, device="cuda")
         ranks = range(P) if a.ranks == "all" else [int(x) for x in a.ranks.split(",") if int(x) < P]
         nch = a.chunks if P > 1 else 1
         for p in ranks:
             t0 = time.time()
-            steps = replay_rank(h, ws, m, n, b, q, k, P, p, nch)
+            steps = replay_rank(h, ws, src, m, n, b, q, k, P, p, nch)
             torch.cuda.synchronize()
             per = []
             for ev, own, mp, np_ in steps:
@@ -188,7 +198,7 @@ def main():
             tot = sum(sum(s[ph] for ph in PHASES) for s in per)
             print(f"P={P} p={p}: compute {tot / 1e3:.3f} s (wall {time.time() - t0:.1f} s)", flush=True)
             out["runs"].append({"P": P, "p": p, "chunks": nch, "steps": per, "compute_s": tot / 1e3})
-        del ws
+        del ws, src
         torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     json.dump(out, open(a.out, "w"))
