@@ -72,6 +72,26 @@ def case_gemm_cfgs():
     print("gemm cfgs 0..5 ok", flush=True)
 
 
+def case_cholqr():
+    """the CholeskyQR2 panel path (R22): forced on every sub-panel of a small solve (whose
+    rank-transition and square panels decline, so the predicated Householder kernels run too),
+    plus a tall panel with a zero column (one sub-panel accepted, one declined)"""
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        case_lstsq()
+    h = utv.default_handle()
+    rng = np.random.default_rng(8)
+    P = rng.standard_normal((3000, 128))
+    P[:, 70] = 0.0
+    Pd, W, tau, T = h.hqr(dev(P))
+    torch.cuda.synchronize()
+    assert float(tau[70]) == 0.0
+    Q = np.eye(3000, 128) - W.cpu().numpy() @ (T.cpu().numpy() @ W.cpu().numpy()[:128].T)
+    R = np.triu(Pd.cpu().numpy())[:128]
+    e = np.linalg.norm(Q @ R - P) / np.linalg.norm(P)
+    assert e < 1e-13, e
+    print(f"cholqr hqr 3000x128 (zero column): ||QR - P|| / ||P|| {e:.1e}", flush=True)
+
+
 def case_wide():
     G = gen.GpMatrix(300, 420, 150, seed=6)
     B, X0 = G.known_rhs(k=1, consistent=True)
@@ -130,7 +150,7 @@ def case_dist_ooc():
 
 
 CASES = {"lstsq": case_lstsq, "lstsq256": case_lstsq_b256, "qrglobal": case_qr_global, "gemm": case_gemm_cfgs,
-         "wide": case_wide, "ooc": case_ooc, "distooc": case_dist_ooc}
+         "wide": case_wide, "ooc": case_ooc, "distooc": case_dist_ooc, "cholqr": case_cholqr}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
