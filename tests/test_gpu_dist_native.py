@@ -355,3 +355,10 @@ def test_local_group_factor_then_solve(utv):
     for x in X:
         assert np.array_equal(x, X[0])
     assert np.linalg.norm(X[0] - Xo) <= 1e-9 * np.linalg.norm(Xo)
+
+
+def test_local_group_cholqr_forced(utv):
+    """The multi-GPU path (QR(Y) on every rank, the owner's a5 panel) with CholeskyQR2 panels forced
+    (R22): X bit-identical on every rank, x to 1e-9 of the oracle, r identical."""
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        test_local_group_matches_oracle(utv, 3, 700, 550, 260, 64, 2, 3)

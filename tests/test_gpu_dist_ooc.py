@@ -155,3 +155,9 @@ def test_dist_streamed_rejects_device_shard(utv):
     finally:
         for h in hs:
             h.close()
+
+
+def test_dist_streamed_cholqr_forced(utv, monkeypatch):
+    """Multi-GPU x out-of-core with CholeskyQR2 panels forced (R22): the same parity bar."""
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        test_dist_streamed_matches_oracle(utv, monkeypatch, 2, 900, 640, 333, 128, 2, 2, 128)

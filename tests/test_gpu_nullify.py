@@ -112,3 +112,9 @@ def test_lstsq_nullify_exact_rank_equals_fast_option(utv):
     Xn, rn = utv.lstsq(dev(G.A), dev(B), utv.Opts(block=32, power_iters=1, seed=3, flags=utv.UTV_NULLIFY_T12))
     assert rs == rn == 120
     assert np.linalg.norm(host(Xs) - host(Xn)) <= 1e-10 * np.linalg.norm(host(Xs))
+
+
+def test_lstsq_nullify_cholqr_forced(utv):
+    """Nullify's blocked RZ panels (R19) and the factorization with CholeskyQR2 forced (R22)."""
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        test_lstsq_nullify_matches_oracle(utv, 400, 330, 300, 128, 1, 3, False)

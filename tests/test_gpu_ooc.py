@@ -188,3 +188,11 @@ def test_streamed_single_block_nan_is_reported(utv, h, monkeypatch, n):
     with pytest.raises(utv.UtvError) as e:
         streamed(utv, h, A, B, 64, 1, 1)
     assert e.value.status == utv.UTV_ERR_NUMERICAL
+
+
+def test_streamed_cholqr_forced(utv, h, monkeypatch):
+    """The out-of-core path with its a3 / a5 panels on CholeskyQR2 + reconstruction wherever that
+    accepts (forced at these heights, R22; the exact-rank transition declines to the Householder
+    kernels on the device): the same parity bar."""
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        test_streamed_lstsq_matches_oracle(utv, h, monkeypatch, 700, 550, 260, 64, 2, 3, 192, True)

@@ -187,3 +187,10 @@ def test_local_group_keep_then_new_rhs(utv, P, m, n, r, b, q):
         assert np.linalg.norm(Xg - Xo) <= 1e-9 * np.linalg.norm(Xo)
     for hd in handles:
         hd.close()
+
+
+def test_keep_then_new_rhs_cholqr_forced(utv, h):
+    """Factor reuse for a new right-hand side with CholeskyQR2 panels forced
+    (R22): the kept W_U / T_U from the reconstruction serve later solves exactly as well."""
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        test_lstsq_keep_then_new_rhs(utv, h, 900, 700, 333, 128, 2, 3, False)

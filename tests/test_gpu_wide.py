@@ -155,3 +155,9 @@ def test_wide_large_known_solution(utv, h):
     assert (torch.linalg.norm(X - X0) / torch.linalg.norm(X0)).item() <= 1e-10
     ne = torch.linalg.norm(A.t() @ (A @ X - Bm)) / (torch.linalg.norm(A) ** 2 * torch.linalg.norm(X))
     assert ne.item() <= 1e-12
+
+
+def test_wide_cholqr_forced(utv, h):
+    """Wide m < n (randUTV of A^T, R21) with CholeskyQR2 panels forced (R22)."""
+    with utv.tuned(utv.UTV_TUNE_QR_CHOLQR, 2):
+        test_wide_matches_oracle(utv, h, 600, 1000, 600, 128, 2, 1, 1.0)
