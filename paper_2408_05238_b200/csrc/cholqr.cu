@@ -308,6 +308,7 @@ cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const doubl
     if (tid == 0) *flag = 4;
     return;
   }
+  CQ_TRACE(5);
   if (lu_fast<false>(a, nb, nullptr, pv) != 0) {       // R_2 = chol(G_2) -> a
     if (tid == 0) *flag = 2;
     return;
@@ -316,6 +317,7 @@ cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const doubl
   CQ_TRACE(1);
   load_cm(R1, nb, nb, b);
   mm(y, a, b, nb, 1.0);                               // y = R = R_2 R_1
+  CQ_TRACE(6);
   for (int e = tid; e < CQ_NB * CQ_NB; e += CQ_THREADS) {   // b = R_2 padded for the row solves
     const int r = e / CQ_NB, c = e % CQ_NB;
     b[r * CQ_LD + c] = (r < nb && c < nb) ? a[r * CQ_LD + c] : 0.0;
@@ -360,6 +362,7 @@ cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const doubl
     b[r * CQ_LD + c] = (in && c > r) ? m[c * CQ_LD + r] : 0.0;
   }
   __syncthreads();
+  CQ_TRACE(7);
   if (tid < 2 * CQ_NB) {                             // row r of T: t L^T = -(U' S)_r (2 threads / row)
     const int r = tid >> 1, h = tid & 1;
     double x[32];
@@ -376,6 +379,7 @@ cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const doubl
       if (r < nb && col == r) tau[r] = x[c];
     }
   }
+  CQ_TRACE(8);
   mm(m, a, y, nb, 1.0);                               // m = M = U' R
   for (int e = tid; e < nb * nb; e += CQ_THREADS) {
     const int r = e % nb, c = e / nb;

@@ -19,7 +19,9 @@ for m, w in ((50000, 64), (50000, 256)):
     torch.cuda.synchronize()
     buf = (C.c_longlong * 16)()
     utv.lib().utv_debug_cqr_trace(buf)
-    t = [buf[i] for i in range(5)]
-    names = ["", "G2 check + chol", "R, Q_top", "LU(sign)", "writes, T, M"]
-    print(f"{m}x{w} recon phases (us):", {names[i]: round((t[i] - t[i - 1]) / 1e3, 2) for i in range(1, 5)},
-          "total", round((t[4] - t[0]) / 1e3, 2))
+    order = [0, 5, 1, 6, 2, 3, 7, 8, 4]
+    names = ["load G2 + check", "chol(G2)", "R = R2 R1 (mm)", "Q_top row solves", "LU(sign)",
+             "P/W writes, U', L^T", "T row solves", "M = U'R (mm) + write"]
+    t = [buf[i] for i in order]
+    print(f"{m}x{w} recon phases (us):", {names[i]: round((t[i + 1] - t[i]) / 1e3, 2) for i in range(len(names))},
+          "total", round((t[-1] - t[0]) / 1e3, 2))
