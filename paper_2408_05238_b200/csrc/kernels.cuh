@@ -65,6 +65,10 @@ void launch_rank(cudaStream_t st, int64_t n, const double* T, int64_t ldt, doubl
 // In place z := T(j0:j1, j0:j1)^{-1} z for the rows j0..j1-1 of Z (ldz), k columns.
 void launch_trsv_block(cudaStream_t st, int64_t j0, int64_t j1, const double* T, int64_t ldt, double* Z, int64_t ldz,
                        int64_t k);
+// In place z := T11^{-1} z (r x k, ldz) for a T11 whose b x b diagonal blocks are DIAGONAL (randUTV
+// without Nullify: A11 := Sigma): one GEMV launch per block + one scaling pass (b <= 256).
+void launch_diag_block_solve(cudaStream_t st, int64_t r, int64_t b, const double* T, int64_t ldt, double* Z,
+                             int64_t ldz, int64_t k);
 
 // ---- misc (misc.cu) ----------------------------------------------------------------------
 void launch_set_identity(cudaStream_t st, int64_t rows, int64_t cols, double* A, int64_t lda);

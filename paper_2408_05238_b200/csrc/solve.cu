@@ -101,7 +101,71 @@ __global__ void __launch_bounds__(TS_ROWS) trsv_block_kernel(int64_t j0, int64_t
     __syncthreads();
   }
 }
+
+// a9 when T11's b x b diagonal blocks are diagonal (randUTV sets A11 := Sigma, so
+// without Nullify T11 = blockdiag(Sigma_i) + strictly-upper blocks): bottom-up over the blocks,
+// block q (rows j0:j1) contributes acc(0:j0) -= T(0:j0, j0:j1) (acc(j0:j1) ./ diag(T)(j0:j1)).
+// acc(j0:j1) is final once the blocks below are in and no later launch writes it, so one pass
+// z = acc ./ diag(T) at the end gives z = T11^{-1} C.  One HBM-bound GEMV launch per block: thread
+// per row, the block's <= 256 columns read coalesced, z_q (scaled redundantly per CTA) in shared memory.
+constexpr int DS_THREADS = 256, DS_K = 16, DS_B = 256;
+__global__ void __launch_bounds__(DS_THREADS) diag_block_gemv_kernel(int64_t j0, int64_t j1,
+                                                                     const double* __restrict__ T, int64_t ldt,
+                                                                     double* __restrict__ Z, int64_t ldz, int64_t k) {
+  __shared__ double zq[DS_K][DS_B];
+  const int bs = (int)(j1 - j0);
+  const int64_t i = (int64_t)blockIdx.x * DS_THREADS + threadIdx.x;
+  for (int64_t c0 = 0; c0 < k; c0 += DS_K) {
+    const int kc = (int)((k - c0) < DS_K ? (k - c0) : DS_K);
+    for (int e = threadIdx.x; e < bs * kc; e += DS_THREADS) {
+      const int q = e % bs, c = e / bs;
+      zq[c][q] = Z[cm(j0 + q, c0 + c, ldz)] / T[cm(j0 + q, j0 + q, ldt)];
+    }
+    __syncthreads();
+    if (i < j0) {
+      double acc[DS_K];
+#pragma unroll
+      for (int c = 0; c < DS_K; ++c) acc[c] = 0.0;
+      const double* Ti = T + cm(i, j0, ldt);
+      for (int q = 0; q < bs; ++q) {
+        const double t = Ti[(size_t)q * ldt];
+#pragma unroll
+        for (int c = 0; c < DS_K; ++c)
+          if (c < kc) acc[c] += t * zq[c][q];
+      }
+#pragma unroll
+      for (int c = 0; c < DS_K; ++c)
+        if (c < kc) Z[cm(i, c0 + c, ldz)] -= acc[c];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void diag_scale_kernel(int64_t r, int64_t k, const double* __restrict__ T, int64_t ldt, double* Z,
+                                  int64_t ldz) {
+  const int64_t total = r * k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % r, c = e / r;
+    Z[cm(i, c, ldz)] /= T[cm(i, i, ldt)];
+  }
+}
 }  // namespace
+
+void launch_diag_block_solve(cudaStream_t st, int64_t r, int64_t b, const double* T, int64_t ldt, double* Z,
+                             int64_t ldz, int64_t k) {
+  if (r <= 0 || k <= 0) return;
+  if (b > DS_B) throw CudaError{cudaErrorInvalidValue, "launch_diag_block_solve: b > 256", __LINE__};
+  for (int64_t j0 = ((r - 1) / b) * b; j0 > 0; j0 -= b) {
+    const int64_t j1 = std::min(r, j0 + b);
+    ProfScope prof(st, kProfSolve, 1, 2.0 * (double)j0 * (j1 - j0) * k, 8.0 * (double)j0 * (j1 - j0) + 16.0 * j0 * k);
+    diag_block_gemv_kernel<<<(unsigned)((j0 + DS_THREADS - 1) / DS_THREADS), DS_THREADS, 0, st>>>(j0, j1, T, ldt, Z,
+                                                                                                  ldz, k);
+    UTV_CUDA(cudaGetLastError());
+  }
+  ProfScope prof(st, kProfSolve, 1, (double)r * k, 16.0 * (double)r * k + 8.0 * r);
+  diag_scale_kernel<<<(unsigned)std::min<int64_t>((r * k + 255) / 256, 1024), 256, 0, st>>>(r, k, T, ldt, Z, ldz);
+  UTV_CUDA(cudaGetLastError());
+}
 
 void launch_rank(cudaStream_t st, int64_t n, const double* T, int64_t ldt, double tau, int64_t* r_dev) {
   ProfScope prof(st, kProfSolve, 1, 0.0, 8.0 * (double)n);

@@ -870,11 +870,16 @@ void solve_factored(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t
   double* Zb = c.at(c.L.zsolve);
   if (!z_ready) {
     launch_copy(st, r, k, Cm, ldc, Zb, r);
-    constexpr int64_t SB = 256;
-    for (int64_t j0 = ((r - 1) / SB) * SB; j0 >= 0; j0 -= SB) {               // z = T11^{-1} C(0:r)
-      const int64_t j1 = std::min(r, j0 + SB);
-      launch_trsv_block(st, j0, j1, T, ldt, Zb, r, k);
-      if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Zb + j0, r, 1.0, Zb, r);
+    if (!ns && b <= 256) {
+      // without Nullify T11's b x b diagonal blocks are Sigma_i (diagonal): GEMVs + one scaling
+      launch_diag_block_solve(st, r, b, T, ldt, Zb, r, k);
+    } else {
+      constexpr int64_t SB = 256;
+      for (int64_t j0 = ((r - 1) / SB) * SB; j0 >= 0; j0 -= SB) {             // z = T11^{-1} C(0:r)
+        const int64_t j1 = std::min(r, j0 + SB);
+        launch_trsv_block(st, j0, j1, T, ldt, Zb, r, k);
+        if (j0 > 0) c.gemm(false, false, j0, k, j1 - j0, -1.0, T + cm(0, j0, ldt), ldt, Zb + j0, r, 1.0, Zb, r);
+      }
     }
   }
   double* tmp = c.at(c.L.Z1);
