@@ -870,7 +870,8 @@ void solve_factored(const Ctx& c, int64_t n, int64_t r, const double* T, int64_t
   double* Zb = c.at(c.L.zsolve);
   if (!z_ready) {
     launch_copy(st, r, k, Cm, ldc, Zb, r);
-    if (!ns && b <= 256) {
+    static const bool force_trsv = [] { const char* e = std::getenv("UTV_SOLVE_TRSV"); return e && e[0] == '1'; }();
+    if ((!ns || ns->i0.empty()) && b <= 256 && !force_trsv) {
       // without Nullify T11's b x b diagonal blocks are Sigma_i (diagonal): GEMVs + one scaling
       launch_diag_block_solve(st, r, b, T, ldt, Zb, r, k);
     } else {
