@@ -417,12 +417,16 @@ void assemble_t(cudaStream_t st, int64_t rows, int64_t c0, int64_t c1, int64_t b
   if (cw <= bw) return;
   const double* Wc = W + cm(c0, c0, ldw);
   double* Tc = T + cm(c0, c0, ldt);
-  dgemm(st, true, false, cw, cw, rows - c0, 1.0, Wc, ldw, Wc, ldw, 0.0, pw.gram, cw, pw.gemm_work,
-        pw.gemm_work_doubles, pw.num_sms);
+  // only the blocks W_i^T W_j with i < j are needed: S' = W(:, 0:jl)^T W(:, bw:cw) (jl = the last
+  // block's first column), element (p, q) = W_p^T W_(q + bw) (44% fewer flops than the full Gram
+  // at 4 sub-panels)
+  const int64_t jl = ((cw - 1) / bw) * bw;
+  dgemm(st, true, false, jl, cw - bw, rows - c0, 1.0, Wc, ldw, Wc + cm(0, bw, ldw), ldw, 0.0, pw.gram, jl,
+        pw.gemm_work, pw.gemm_work_doubles, pw.num_sms);
   for (int64_t jb = bw; jb < cw; jb += bw) {
     const int64_t nb = std::min<int64_t>(bw, cw - jb);
-    dgemm(st, false, false, jb, nb, nb, 1.0, pw.gram + cm(0, jb, cw), cw, Tc + cm(jb, jb, ldt), ldt, 0.0, pw.x, jb,
-          pw.gemm_work, pw.gemm_work_doubles, pw.num_sms);
+    dgemm(st, false, false, jb, nb, nb, 1.0, pw.gram + cm(0, jb - bw, jl), jl, Tc + cm(jb, jb, ldt), ldt, 0.0, pw.x,
+          jb, pw.gemm_work, pw.gemm_work_doubles, pw.num_sms);
     dgemm(st, false, false, jb, nb, jb, -1.0, Tc, ldt, pw.x, jb, 0.0, Tc + cm(0, jb, ldt), ldt, pw.gemm_work,
           pw.gemm_work_doubles, pw.num_sms);
   }
