@@ -83,9 +83,11 @@ utv_status utv_rank_diag(utv_handle handle, int64_t n, const double* d, double t
  *   UTV_TUNE_SVD_LAG      multi-GPU handles: steps (1..8) by which the application of a diagonal
  *                         block's SVD may trail its panel QR (0 = automatic: 1 at P = 1, else 8)
  *   UTV_TUNE_QR_CHOLQR    a3/a5 panel algorithm: 0 = automatic (CholeskyQR2 + Householder
- *                         reconstruction on 64-column sub-panels of >= 2048 rows, the Householder
- *                         sub-panel kernels where it declines; reading R22), 1 = Householder kernels
- *                         only, 2 = CholeskyQR2 attempted at any panel height
+ *                         reconstruction on 64-column sub-panels of >= 2048 rows -- a last
+ *                         sub-panel narrower than 48 columns excepted --, the Householder sub-panel
+ *                         kernels where it declines, chosen on the device; reading R22),
+ *                         1 = Householder kernels only, 2 = CholeskyQR2 attempted on every
+ *                         sub-panel at any height and width
  * Returns UTV_ERR_ARG for an unknown key; *old (if non-NULL) gets the previous value. */
 enum {
   UTV_TUNE_GEMM_CFG = 1,
