@@ -106,15 +106,19 @@ __global__ void __launch_bounds__(TS_ROWS) trsv_block_kernel(int64_t j0, int64_t
 // without Nullify T11 = blockdiag(Sigma_i) + strictly-upper blocks): bottom-up over the blocks,
 // block q (rows j0:j1) contributes acc(0:j0) -= T(0:j0, j0:j1) (acc(j0:j1) ./ diag(T)(j0:j1)).
 // acc(j0:j1) is final once the blocks below are in and no later launch writes it, so one pass
-// z = acc ./ diag(T) at the end gives z = T11^{-1} C.  One HBM-bound GEMV launch per block: thread
-// per row, the block's <= 256 columns read coalesced, z_q (scaled redundantly per CTA) in shared memory.
-constexpr int DS_THREADS = 256, DS_K = 16, DS_B = 256;
+// z = acc ./ diag(T) at the end gives z = T11^{-1} C.  One HBM-bound GEMV launch per block, z_q
+// (scaled redundantly per CTA) in shared memory.
+constexpr int DS_THREADS = 256, DS_K = 8, DS_B = 256, DS_ROWS = 32, DS_WARPS = DS_THREADS / 32;
+// CTA = 32 rows (lane = row, each warp column load is one coalesced 256-byte segment) x the block's
+// columns split over the 8 warps, then a fixed-order reduction of the 8 partial sums.
 __global__ void __launch_bounds__(DS_THREADS) diag_block_gemv_kernel(int64_t j0, int64_t j1,
                                                                      const double* __restrict__ T, int64_t ldt,
                                                                      double* __restrict__ Z, int64_t ldz, int64_t k) {
   __shared__ double zq[DS_K][DS_B];
+  __shared__ double red[DS_WARPS][DS_K][DS_ROWS];
   const int bs = (int)(j1 - j0);
-  const int64_t i = (int64_t)blockIdx.x * DS_THREADS + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * DS_ROWS + lane;
   for (int64_t c0 = 0; c0 < k; c0 += DS_K) {
     const int kc = (int)((k - c0) < DS_K ? (k - c0) : DS_K);
     for (int e = threadIdx.x; e < bs * kc; e += DS_THREADS) {
@@ -122,20 +126,30 @@ __global__ void __launch_bounds__(DS_THREADS) diag_block_gemv_kernel(int64_t j0,
       zq[c][q] = Z[cm(j0 + q, c0 + c, ldz)] / T[cm(j0 + q, j0 + q, ldt)];
     }
     __syncthreads();
-    if (i < j0) {
-      double acc[DS_K];
+    double acc[DS_K];
 #pragma unroll
-      for (int c = 0; c < DS_K; ++c) acc[c] = 0.0;
+    for (int c = 0; c < DS_K; ++c) acc[c] = 0.0;
+    if (i < j0) {
       const double* Ti = T + cm(i, j0, ldt);
-      for (int q = 0; q < bs; ++q) {
-        const double t = Ti[(size_t)q * ldt];
+#pragma unroll 4
+      for (int q = warp; q < bs; q += DS_WARPS) {
+        const double t = __ldg(Ti + (size_t)q * ldt);
 #pragma unroll
         for (int c = 0; c < DS_K; ++c)
           if (c < kc) acc[c] += t * zq[c][q];
       }
+    }
 #pragma unroll
-      for (int c = 0; c < DS_K; ++c)
-        if (c < kc) Z[cm(i, c0 + c, ldz)] -= acc[c];
+    for (int c = 0; c < DS_K; ++c)
+      if (c < kc) red[warp][c][lane] = acc[c];
+    __syncthreads();
+    if (warp == 0 && i < j0) {
+      for (int c = 0; c < kc; ++c) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < DS_WARPS; ++w) sum += red[w][c][lane];
+        Z[cm(i, c0 + c, ldz)] -= sum;
+      }
     }
     __syncthreads();
   }
@@ -158,8 +172,8 @@ void launch_diag_block_solve(cudaStream_t st, int64_t r, int64_t b, const double
   for (int64_t j0 = ((r - 1) / b) * b; j0 > 0; j0 -= b) {
     const int64_t j1 = std::min(r, j0 + b);
     ProfScope prof(st, kProfSolve, 1, 2.0 * (double)j0 * (j1 - j0) * k, 8.0 * (double)j0 * (j1 - j0) + 16.0 * j0 * k);
-    diag_block_gemv_kernel<<<(unsigned)((j0 + DS_THREADS - 1) / DS_THREADS), DS_THREADS, 0, st>>>(j0, j1, T, ldt, Z,
-                                                                                                  ldz, k);
+    diag_block_gemv_kernel<<<(unsigned)((j0 + DS_ROWS - 1) / DS_ROWS), DS_THREADS, 0, st>>>(j0, j1, T, ldt, Z, ldz,
+                                                                                            k);
     UTV_CUDA(cudaGetLastError());
   }
   ProfScope prof(st, kProfSolve, 1, (double)r * k, 16.0 * (double)r * k + 8.0 * r);
