@@ -19,7 +19,6 @@
 //  * Deterministic split-K for skinny outputs with long K (panel Gram/projection products):
 //    partials to a workspace, reduced in a fixed order by dgemm_splitk_reduce.
 #include "gemm.cuh"
-#include <cstring>
 #include "prof.cuh"
 #include <cuda.h>            // CUtensorMap (type only; the encoder is fetched from the driver at run time)
 #include <cmath>
@@ -375,11 +374,6 @@ struct TmaCfg {
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024;   // + alignment slack
   static_assert(STAGES >= 3, "not enough shared memory for a 3-stage pipeline");
-  // C prefetch (beta != 0): the C tile is TMA-loaded, as boxes {BM rows, CB columns} of one stage
-  // each, into the pipeline slots the last k-tiles free, so the epilogue reads C from shared memory
-  static constexpr int CB = STAGE_BYTES / (BM * 8);
-  static constexpr int C_BOXES = (CB > 0 && CB <= 256 && BN % CB == 0) ? BN / CB : 0;
-  static constexpr bool C_PRE = C_BOXES > 0 && C_BOXES <= STAGES - 1;
 };
 
 template <int BMN, bool MN_MAJOR>
@@ -393,10 +387,9 @@ __device__ __forceinline__ double tma_frag(const char* s, int mn, int k) {
 
 template <bool TA, bool TB, int ID>
 __global__ void __launch_bounds__(TmaCfg<TA, TB, ID>::THREADS, TmaCfg<TA, TB, ID>::CTAS_PER_SM)
-dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmC, int64_t M, int64_t N, int64_t K, double alpha, double beta,
-                 double* __restrict__ C, int64_t ldc, int64_t k_chunk, double* __restrict__ partial, int mn_3d,
-                 int cpre_in, Pred pr) {
+dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
+                 int64_t N, int64_t K, double alpha, double beta, double* __restrict__ C, int64_t ldc,
+                 int64_t k_chunk, double* __restrict__ partial, int mn_3d, Pred pr) {
   if (pred_skip(pr)) return;
   using CF = TmaCfg<TA, TB, ID>;
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES;
@@ -404,7 +397,7 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   constexpr bool A_MN = CF::A_MN, B_MN = CF::B_MN;
   constexpr int NWARPS = CF::THREADS / 32;
   extern __shared__ __align__(1024) char smem_raw[];
-  __shared__ uint64_t full[STAGES], empty[STAGES], cfull[CF::C_BOXES > 0 ? CF::C_BOXES : 1];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
   // 1024-byte aligned (SWIZZLE_128B); offsetting the __shared__ array keeps LDS addressing
   char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
@@ -419,9 +412,6 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int64_t kbeg = (int64_t)blockIdx.z * k_chunk;
   const int64_t kend = min(K, kbeg + k_chunk);
   const int nkt = (int)((kend - kbeg + BK - 1) / BK);
-  // C prefetch: box b goes into the slot k-tile nkt - STAGES + b used (freed at iteration
-  // nkt - STAGES + 1 + b, when no k-tile load is left to issue)
-  const bool cpre = CF::C_PRE && cpre_in && !partial && beta != 0.0 && nkt >= STAGES;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -444,8 +434,6 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARPS);
     }
-#pragma unroll
-    for (int b = 0; b < CF::C_BOXES; ++b) mbar_init(&cfull[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
@@ -501,13 +489,6 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (tid == 0 && kt + STAGES - 1 < nkt) {
           if (kt > 0) mbar_wait(&empty[(kt - 1) % STAGES], (unsigned)(((kt - 1) / STAGES) & 1));
           issue(kt + STAGES - 1);
-        } else if constexpr (CF::C_PRE) {
-          const int b = kt - (nkt - STAGES + 1);          // C box b into the slot of k-tile kt-1
-          if (tid == 0 && cpre && b >= 0 && b < CF::C_BOXES) {
-            mbar_wait(&empty[(kt - 1) % STAGES], (unsigned)(((kt - 1) / STAGES) & 1));
-            mbar_expect_tx(&cfull[b], (unsigned)(BM * CF::CB * 8));
-            tma_load_2d(stage_a((kt - 1) % STAGES), &tmC, &cfull[b], m0, n0 + b * CF::CB);
-          }
         }
         if (kt + 1 < nkt) {
           const int s1 = (kt + 1) % STAGES;
@@ -537,24 +518,7 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (m < M && n < N) P[cm(m, n, M)] = acc[i][j][r];
         }
   } else {
-    if (cpre) {
-      // C from the prefetched boxes: local (ml, nl) in box nl / CB, column-major {BM, CB}
-#pragma unroll
-      for (int b = 0; b < CF::C_BOXES; ++b) mbar_wait(&cfull[b], 0);
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int ml = wm * WTM + i * 16 + g + (r >> 1) * 8;
-            const int nl = wn * WTN + j * 8 + 2 * t + (r & 1);
-            const int b = nl / CF::CB;
-            const double c = *reinterpret_cast<const double*>(stage_a((nkt - STAGES + b) % STAGES) +
-                                                              ((size_t)(nl % CF::CB) * BM + ml) * 8);
-            acc[i][j][r] = alpha * acc[i][j][r] + beta * c;
-          }
-    } else if (beta != 0.0) {
+    if (beta != 0.0) {
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -674,29 +638,12 @@ bool launch_tma_t(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   if (!make_tmap(&tb_map, B, TB ? N : K, TB ? K : N, ldb, TB, CF::BN, &b3)) return false;
   static const int group_m = [] { const char* e = std::getenv("UTV_GEMM_GROUP_M"); return e ? std::atoi(e) : 0; }();
   const int mn_3d = (a3 ? 1 : 0) | (b3 ? 2 : 0) | (group_m << 8);
-  // C prefetch through TMA (beta != 0, no split-K, 16-byte aligned C): UTV_GEMM_CPRE=0 disables it
-  static const bool cpre_env = [] { const char* e = std::getenv("UTV_GEMM_CPRE"); return !(e && e[0] == '0'); }();
-  CUtensorMap tc_map;
-  std::memset(&tc_map, 0, sizeof(tc_map));
-  int cpre = 0;
-  if constexpr (CF::C_PRE) {
-    if (cpre_env && beta != 0.0 && splits == 1 && reinterpret_cast<uintptr_t>(C) % 16 == 0 && ldc % 2 == 0) {
-      EncodeTiledFn fn = encode_fn();
-      const cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
-      const cuuint64_t strides[1] = {(cuuint64_t)ldc * 8};
-      const cuuint32_t box[2] = {(cuuint32_t)CF::BM, (cuuint32_t)CF::CB};
-      const cuuint32_t estr[2] = {1, 1};
-      cpre = fn && fn(&tc_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, C, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    }
-  }
   static std::atomic<unsigned long long> attr_set{0};
   auto kern = dgemm_tma_kernel<TA, TB, ID>;
   ensure_smem_attr(kern, (int)CF::SMEM, attr_set);
   dim3 grid((unsigned)(((N + CF::BN - 1) / CF::BN) * ((M + CF::BM - 1) / CF::BM)), 1u, (unsigned)splits);
-  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(ta_map, tb_map, tc_map, M, N, K, alpha, beta, C, ldc, kc, partial, mn_3d,
-                                            cpre, launch_pred());
+  kern<<<grid, CF::THREADS, CF::SMEM, st>>>(ta_map, tb_map, M, N, K, alpha, beta, C, ldc, kc, partial, mn_3d,
+                                            launch_pred());
   UTV_CUDA(cudaGetLastError());
   return true;
 }
