@@ -12,11 +12,12 @@
 // R = R_2 R_1), and W_2 = Q_2 U'^{-1} = P_2 (U' R)^{-1}.  Per sub-panel: two skinny DMMA Gram GEMMs
 // over the R rows (P^T P, Q_1^T Q_1), two row-parallel triangular solves over the R rows
 // (cqr_trsm_kernel: P R_1^{-1}, P_2 (U' R)^{-1}, substitution in registers), two single-CTA
-// nb x nb kernels (Cholesky / LU with one CTA barrier per column, row solves, products) and one host
-// wait for the accept flag -- no per-column grid barrier, no explicit triangular inverse.
-// CholeskyQR2 is accurate only while kappa(P) is moderate: a non-positive Cholesky pivot, or a
-// first pass with ||Q_1^T Q_1 - I||_F > 1e-4 (kappa(P) beyond ~1e6), declines the sub-panel, and the
-// host factors it with the Householder kernels instead (panel_qr.cu).  Rank-deficient panels (the
+// nb x nb kernels (Cholesky / LU with one CTA barrier per column, row solves, products) -- no
+// per-column grid barrier, no explicit triangular inverse, no host wait.  CholeskyQR2 is accurate
+// only while kappa(P) is moderate: a non-positive Cholesky pivot, or a first pass with
+// ||Q_1^T Q_1 - I||_F > 1e-4 (kappa(P) beyond ~1e6), declines the sub-panel -- a device flag, which
+// makes the rest of this sequence return at entry and the Householder kernels the caller enqueued
+// behind it (panel_qr.cu, under PredScope) run instead.  Rank-deficient panels (the
 // exact-rank transition of randUTV, zero columns) always take the Householder path, which keeps the
 // paper's tau = 0 convention for zero columns; so do sub-panels with a column whose part below the
 // diagonal vanishes (an LU pivot of magnitude 1), where dlarfg does not reflect.

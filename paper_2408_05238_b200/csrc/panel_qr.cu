@@ -12,7 +12,10 @@
 //    every CTA in a fixed order (deterministic, no atomics on data).
 //  * between sub-panels: the block reflector is applied to the rest of the panel with three
 //    DMMA GEMMs (W^T P, T^T ., P -= W .), and the off-diagonal blocks of T are assembled from
-//    the Gram matrix W^T W:  T_12 = -T_11 (W_1^T W_2) T_22.
+//    the needed blocks of the Gram matrix W^T W:  T_12 = -T_11 (W_1^T W_2) T_22.
+// Tall panels (>= 2048 rows) first try CholeskyQR2 + Householder reconstruction on 64-column
+// sub-panels (cholqr.cu, reading R22): both algorithms are enqueued and a device flag selects
+// one, so the host never waits (the kernels of the other return at entry).
 #include "kernels.cuh"
 #include "prof.cuh"
 #include <cstdlib>
