@@ -201,18 +201,6 @@ __device__ void lu_to_chol(double* a, int nb) {
   __syncthreads();
 }
 
-// Load an nb x nb upper triangular M (column-major, ld) into shared memory padded to CQ_NB with
-// zeros (and minv = 1) beyond nb; minv[k] = 1 / M_kk.
-__device__ void load_upper_padded(const double* __restrict__ g, int64_t ld, int nb, double* M, double* minv) {
-  for (int e = threadIdx.x; e < CQ_NB * CQ_NB; e += CQ_THREADS) {
-    const int r = e % CQ_NB, c = e / CQ_NB;
-    M[r * CQ_LD + c] = (r < nb && c < nb && r <= c) ? g[(size_t)c * ld + r] : 0.0;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < CQ_NB; k += CQ_THREADS) minv[k] = k < nb ? 1.0 / M[k * CQ_LD + k] : 1.0;
-  __syncthreads();
-}
-
 // Kernel 1: R_1 = chol(G_1) (column-major, zeros below); flag = 0 (accepted) or 1 (a non-positive
 // or non-finite pivot: the Householder path).
 __global__ void __launch_bounds__(CQ_THREADS, 1)
@@ -238,12 +226,40 @@ cqr_chol_kernel(int nb, const double* __restrict__ G, int64_t ldg, double* __res
 // the substitution in registers (solve_row_upper2).  Skipped when the flag is set.  In place
 // allowed (X == P): each thread reads its half row before the pair writes.
 constexpr int TRSM_THREADS = 128;
-__global__ void __launch_bounds__(TRSM_THREADS, 4)
+template <bool WITH_T>
+__global__ void __launch_bounds__(TRSM_THREADS)
 cqr_trsm_kernel(int64_t rows, int nb, const double* P, int64_t ldp, const double* __restrict__ M, int ldm,
-                double* X, int64_t ldx, const int* __restrict__ flag) {
+                double* X, int64_t ldx, const int* __restrict__ flag, const double* __restrict__ LU,
+                const double* __restrict__ sg, double* __restrict__ T, int64_t ldt, double* __restrict__ tau) {
   if (*(volatile const int*)flag != 0) return;
   __shared__ double Ms[CQ_NB * CQ_LD];
   __shared__ double minv[CQ_NB];
+  if (WITH_T && blockIdx.x == gridDim.x - 1) {
+    // side job of the last CTA (overlaps the row passes of the others): T = -U' S L^{-T} of the
+    // reconstruction by row solves t_r L^T = -(U' S)_r, from the LU (col-major, ld CQ_NB) and signs
+    for (int e = threadIdx.x; e < CQ_NB * CQ_NB; e += TRSM_THREADS) {   // Ms = L^T (unit, padded)
+      const int r = e / CQ_NB, c = e % CQ_NB;
+      Ms[r * CQ_LD + c] = (r < nb && c < nb && c > r) ? LU[(size_t)r * CQ_NB + c] : 0.0;
+    }
+    for (int k = threadIdx.x; k < CQ_NB; k += TRSM_THREADS) minv[k] = 1.0;
+    __syncthreads();
+    const int r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    double x[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const int col = 32 * h + c;
+      x[c] = (r < nb && col < nb && col >= r) ? -LU[(size_t)col * CQ_NB + r] * sg[col] : 0.0;
+    }
+    solve_row_upper2<true>(x, Ms, minv);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const int col = 32 * h + c;
+      if (r < nb && col < nb) T[(size_t)col * ldt + r] = col >= r ? x[c] : 0.0;
+      if (r < nb && col == r) tau[r] = x[c];
+    }
+    return;
+  }
+  const unsigned nrow_ctas = WITH_T ? gridDim.x - 1 : gridDim.x;
   for (int e = threadIdx.x; e < CQ_NB * CQ_NB; e += TRSM_THREADS) {
     const int r = e % CQ_NB, c = e / CQ_NB;
     Ms[r * CQ_LD + c] = (r < nb && c < nb && r <= c) ? M[(size_t)c * ldm + r] : 0.0;
@@ -254,7 +270,7 @@ cqr_trsm_kernel(int64_t rows, int nb, const double* P, int64_t ldp, const double
   const int h = threadIdx.x & 1;
   constexpr int RPB = TRSM_THREADS / 2;                 // rows per CTA pass
   const int64_t npass = (rows + RPB - 1) / RPB;
-  for (int64_t ps = blockIdx.x; ps < npass; ps += gridDim.x) {   // uniform per CTA (shuffles)
+  for (int64_t ps = blockIdx.x; ps < npass; ps += nrow_ctas) {   // uniform per CTA (shuffles)
     const int64_t i = ps * RPB + (threadIdx.x >> 1);
     const bool live = i < rows;
     double x[32];
@@ -276,13 +292,14 @@ cqr_trsm_kernel(int64_t rows, int nb, const double* P, int64_t ldp, const double
 // nearly orthonormal first pass, i.e. kappa(P) below ~1e6), R_2 = chol(G_2), R = R_2 R_1,
 // Q_top = Q_1top R_2^{-1}, the LU of Q_top - S with the dlarfg signs, then the outputs of the
 // sub-panel's top nb rows:  P top block := S R (upper, zeros below), W top block := L (unit lower),
-// rows above the sub-panel of W := 0, T := -U' S L^{-T} (row solves T L^T = -U' S), tau := diag(T),
-// M := U' R (column-major, for W_2 = P_2 M^{-1}).
+// rows above the sub-panel of W := 0, M := U' R (column-major, for W_2 = P_2 M^{-1}), and the LU
+// (column-major, ld CQ_NB) + signs from which the W_2 launch's extra CTA forms T = -U' S L^{-T} and
+// tau = diag(T) (row solves T L^T = -U' S) while the other CTAs solve the rows.
 __global__ void __launch_bounds__(CQ_THREADS, 1)
 cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const double* __restrict__ Q1, int64_t ldq,
                  const double* __restrict__ R1, int* __restrict__ flag, double* __restrict__ P, int64_t ldp,
-                 double* __restrict__ W, int64_t ldw, int64_t wtop, double* __restrict__ tau, double* __restrict__ T,
-                 int64_t ldt, double* __restrict__ Mout) {
+                 double* __restrict__ W, int64_t ldw, int64_t wtop, double* __restrict__ Mout,
+                 double* __restrict__ LUout, double* __restrict__ Sout) {
   if (*(volatile int*)flag != 0) return;
   extern __shared__ double sm[];
   double* a = sm;
@@ -356,30 +373,15 @@ cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const doubl
     const int64_t i = e % wtop, c = e / wtop;
     W[c * ldw + (i - wtop)] = 0.0;
   }
-  for (int e = tid; e < CQ_NB * CQ_NB; e += CQ_THREADS) {   // a = U' (zeros below), b = L^T (unit, padded)
-    const int r = e / CQ_NB, c = e % CQ_NB;
+  for (int e = tid; e < CQ_NB * CQ_NB; e += CQ_THREADS) {   // a = U' (zeros below); the LU and the
+    const int r = e / CQ_NB, c = e % CQ_NB;                  // signs for the T side job (trsm kernel)
     const bool in = r < nb && c < nb;
     a[r * CQ_LD + c] = (in && c >= r) ? m[r * CQ_LD + c] : 0.0;
-    b[r * CQ_LD + c] = (in && c > r) ? m[c * CQ_LD + r] : 0.0;
+    LUout[(size_t)c * CQ_NB + r] = in ? m[r * CQ_LD + c] : 0.0;
   }
+  for (int k = tid; k < CQ_NB; k += CQ_THREADS) Sout[k] = k < nb ? s[k] : 1.0;
   __syncthreads();
   CQ_TRACE(7);
-  if (tid < 2 * CQ_NB) {                             // row r of T: t L^T = -(U' S)_r (2 threads / row)
-    const int r = tid >> 1, h = tid & 1;
-    double x[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const int col = 32 * h + c;
-      x[c] = (r < nb && col < nb) ? -a[r * CQ_LD + col] * s[col] : 0.0;
-    }
-    solve_row_upper2<true>(x, b, minv);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const int col = 32 * h + c;
-      if (r < nb && col < nb) T[(size_t)col * ldt + r] = col >= r ? x[c] : 0.0;
-      if (r < nb && col == r) tau[r] = x[c];
-    }
-  }
   CQ_TRACE(8);
   mm(m, a, y, nb, 1.0);                               // m = M = U' R
   for (int e = tid; e < nb * nb; e += CQ_THREADS) {
@@ -394,7 +396,7 @@ cqr_recon_kernel(int nb, const double* __restrict__ G2, int64_t ldg, const doubl
 
 int cholqr_max_width() { return CQ_NB; }
 
-size_t cholqr_small_doubles() { return 3 * (size_t)CQ_NB * CQ_NB; }
+size_t cholqr_small_doubles() { return 4 * (size_t)CQ_NB * CQ_NB + CQ_NB; }
 
 // Enqueue the CholeskyQR2 + reconstruction of columns [jb, jb + nb) of the panel (rows jb:rows).
 // On the device, pw.dflag ends 0 (accepted: P, W, T, tau written) or nonzero (declined: nothing of
@@ -408,6 +410,8 @@ void cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* 
   double* G = pw.csm;
   double* R1 = G + CQ_NB * CQ_NB;
   double* M = R1 + CQ_NB * CQ_NB;
+  double* LU = M + CQ_NB * CQ_NB;              // the signed LU of Q_top - S and the signs (T side job)
+  double* Sg = LU + CQ_NB * CQ_NB;
   const size_t smem1 = (size_t)CQ_MAT * sizeof(double), smem2 = 4 * (size_t)CQ_MAT * sizeof(double);
   static std::atomic<unsigned long long> attr1{0}, attr2{0};
   ensure_smem_attr(cqr_chol_kernel, (int)smem1, attr1);
@@ -424,7 +428,8 @@ void cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* 
     ProfScope prof(st, kProfPanel, 1, (double)R * nb * nb, 16.0 * (double)R * nb);
     prof.shape(R, nb, 1, 12);
     const int64_t blocks = std::min<int64_t>((R + TRSM_THREADS / 2 - 1) / (TRSM_THREADS / 2), 8 * (int64_t)pw.num_sms);
-    cqr_trsm_kernel<<<(unsigned)blocks, TRSM_THREADS, 0, st>>>(R, nb, Pb, ldp, R1, nb, pw.cq, R, pw.dflag);
+    cqr_trsm_kernel<false><<<(unsigned)blocks, TRSM_THREADS, 0, st>>>(R, nb, Pb, ldp, R1, nb, pw.cq, R, pw.dflag,
+                                                                      nullptr, nullptr, nullptr, 0, nullptr);
     UTV_CUDA(cudaGetLastError());                                               // Q_1 = P R_1^{-1}
   }
   dgemm(st, true, false, nb, nb, R, 1.0, pw.cq, R, pw.cq, R, 0.0, G, nb, pw.gemm_work, pw.gemm_work_doubles,
@@ -432,17 +437,22 @@ void cholqr_subpanel(cudaStream_t st, int64_t rows, int64_t jb, int nb, double* 
   {
     ProfScope prof(st, kProfPanel, 1, 3.0 * nb * nb * nb, 40.0 * nb * nb);
     prof.shape(nb, nb, 1, 11);
-    cqr_recon_kernel<<<1, CQ_THREADS, smem2, st>>>(nb, G, nb, pw.cq, R, R1, pw.dflag, Pb, ldp, Wb, ldw, jb, tau + jb,
-                                                   T + cm(jb, jb, ldt), ldt, M);
+    cqr_recon_kernel<<<1, CQ_THREADS, smem2, st>>>(nb, G, nb, pw.cq, R, R1, pw.dflag, Pb, ldp, Wb, ldw, jb, M, LU,
+                                                   Sg);
+    UTV_CUDA(cudaGetLastError());
+  }
+  {
+    // W_2 = P_2 (U' R)^{-1}, and on one extra CTA T = -U' S L^{-T}, tau (overlapping the row passes)
+    ProfScope prof(st, kProfPanel, 1, (double)(R - nb) * nb * nb, 16.0 * (double)(R - nb) * nb);
+    prof.shape(R - nb, nb, 1, 12);
+    const int64_t blocks =
+        std::min<int64_t>((R - nb + TRSM_THREADS / 2 - 1) / (TRSM_THREADS / 2), 8 * (int64_t)pw.num_sms) + 1;
+    cqr_trsm_kernel<true><<<(unsigned)blocks, TRSM_THREADS, 0, st>>>(R - nb, nb, Pb + nb, ldp, M, nb, Wb + nb, ldw,
+                                                                     pw.dflag, LU, Sg, T + cm(jb, jb, ldt), ldt,
+                                                                     tau + jb);
     UTV_CUDA(cudaGetLastError());
   }
   if (R > nb) {
-    ProfScope prof(st, kProfPanel, 1, (double)(R - nb) * nb * nb, 16.0 * (double)(R - nb) * nb);
-    prof.shape(R - nb, nb, 1, 12);
-    const int64_t blocks = std::min<int64_t>((R - nb + TRSM_THREADS / 2 - 1) / (TRSM_THREADS / 2), 8 * (int64_t)pw.num_sms);
-    cqr_trsm_kernel<<<(unsigned)blocks, TRSM_THREADS, 0, st>>>(R - nb, nb, Pb + nb, ldp, M, nb, Wb + nb, ldw,
-                                                               pw.dflag);    // W_2 = P_2 (U' R)^{-1}
-    UTV_CUDA(cudaGetLastError());
     PredScope accepted(pw.dflag, 0);
     launch_set_zero(st, R - nb, nb, Pb + nb, ldp);
   }
