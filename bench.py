@@ -103,8 +103,9 @@ def hbm_kernels(prof):
     K9 solve, misc copies): ALGORITHMIC bytes recorded per launch / summed launch time."""
     peak, src = hbm_peak()
     out = {"peak_gbs": peak, "peak_source": src,
-           "note": "panel QR and solve are latency-bound (per-column / per-block dependencies), "
-                   "so their fraction of HBM peak is low by construction"}
+           "note": "the panel QR is latency-bound (per-column chains on one CTA or across the grid), so "
+                   "its fraction of HBM peak is low by construction; the solve is one HBM-bound GEMV per "
+                   "block of T11 (its diagonal blocks are the blocks' Sigma)"}
     for fam in ("sketch", "panel", "solve", "misc"):
         v = prof.get(fam)
         if v and v["ms"] > 0 and v["bytes"] > 0:
